@@ -1,0 +1,1022 @@
+/*
+ * noc_oracle.c -- TEST INFRASTRUCTURE ONLY (see noc_oracle.h).
+ *
+ * A plain, slow, obviously-correct, single-threaded CPU simulator of the
+ * per-cycle, per-node step of the paper's simulator (Kumar & Sahu,
+ * arXiv 1508.03235):
+ *   - array-of-structs state, exactly the paper's serial structure
+ *     "for(i..RouterCount) Phase1(i); Phase2(i); Phase3(i)";
+ *   - Phase 1 = core memory-access state machine,
+ *     Phase 2 = age sort + port assignment / deflection,
+ *     Phase 3 = eject / reassemble / service / transfer;
+ *   - the LSPD directory protocol of Fig. 4 with the readings
+ *     R1..R35 of DESIGN.md section 3.
+ * No blocking, no fusion, no bit packing, no SIMD, no threads.  It shares no
+ * code with the CUDA library; only the written model
+ * is common.
+ */
+#include "noc_oracle.h"
+
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Router port order N, S, E, W = Input[0..3]; 4 = eject link X */
+enum { DIR_N = 0, DIR_S = 1, DIR_E = 2, DIR_W = 3, PORT_EJECT = 4 };
+/* message kinds: Table I + readings R16, R18, R13 */
+enum { K_PROBE = 0, K_DA = 1, K_DR = 2, K_NDR = 3, K_RQ = 4, K_RA = 5, K_TRAP = 6, K_EV = 7 };
+/* core modes ("miss under a miss is not allowed"; DESIGN 3.4) */
+enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4 };
+
+#define HOLDER_NONE 0xFFFFFFFFu
+#define AGE_MAX     65535u   /* R32: field width of the deflection age */
+#define PEND_MAX    1023u    /* R32: field width of the pending-EV count */
+
+typedef struct {
+    int present;
+    uint32_t dst, src, kind, fid;   /* struct Flit: DstX/Y, SrcX/Y, FlitId */
+    uint64_t age;                   /* "incremented ... each time when it get deflected" */
+    uint64_t inj;                   /* injection cycle (R1, R2) */
+    uint32_t payload;               /* tag T or holder id (no FlitData, R18) */
+} Flit;
+
+typedef struct { uint32_t kind, dst, payload, nfl; } Packet;   /* ToBeSend entry */
+
+typedef struct { int valid; uint32_t tag; uint64_t stamp; } Line;  /* L2 line */
+
+typedef struct { uint32_t holder; uint32_t pend; } LocEntry;     /* location array */
+
+typedef struct {
+    Flit in[4];        /* Router.Input[4]: flits to be read this cycle        */
+    Flit nin[4];       /* inputs of the next cycle, written by neighbours      */
+    int has_ej;        /* Router.XToProc: the flit ejected this cycle          */
+    Flit ej;
+    Packet *fifo;      /* Core.ToBeSend as a FIFO of packets (R21)             */
+    uint32_t head, count, next;   /* next = NextFlitAddress          */
+    int mode;          /* Core.Wait, refined (DESIGN 3.4)                      */
+    uint64_t ready, start;
+    uint32_t tag;
+    int install;
+    uint32_t rx;       /* Core.ReOrderBuffer, reduced to a counter (R20)       */
+    Line *l2;          /* Core.L2 LSPDSlice                                    */
+    uint64_t script_pos, script_end;
+    uint64_t script_used;
+} Node;
+
+struct orc_sim {
+    orc_config cfg;
+    uint32_t W, H, N;
+    uint64_t t;
+    Node *nodes;
+    Packet *fifo_store;
+    Line *l2_store;
+    LocEntry *loc;
+    uint64_t ntags;
+    orc_event *script;
+    orc_counters c;
+    uint64_t *hl, *hd, *ha;
+    int gen_enabled;
+    int debug;
+    int err;
+};
+
+static __thread char g_err[512];
+static void set_err(const char *msg) { snprintf(g_err, sizeof g_err, "%s", msg); }
+const char *orc_last_error(void) { return g_err; }
+
+static void fail(orc_sim *s, int code, const char *msg)
+{
+    if (s->err == 0) {
+        s->err = code;
+        snprintf(g_err, sizeof g_err, "cycle %llu: %s", (unsigned long long)s->t, msg);
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * Philox4x32-10 (Salmon et al., SC'11; Random123 constants).  Reading R25:
+ * the trace source of P:L233 is replaced by a counter-based generator keyed on
+ * (seed, node, cycle).
+ * ---------------------------------------------------------------------- */
+void orc_philox(uint32_t k0, uint32_t k1, const uint32_t cin[4], uint32_t out[4])
+{
+    uint32_t c0 = cin[0], c1 = cin[1], c2 = cin[2], c3 = cin[3];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static void draw(const orc_sim *s, uint32_t n, uint64_t t, uint32_t r[4])
+{
+    uint32_t ctr[4] = { n, (uint32_t)t, (uint32_t)(t >> 32), 0u };
+    orc_philox((uint32_t)s->cfg.seed, (uint32_t)(s->cfg.seed >> 32), ctr, r);
+}
+
+/* mulhi(r, m) = floor(r * m / 2^32): an integer draw in [0, m) (R25) */
+static uint32_t mulhi(uint32_t r, uint32_t m) { return (uint32_t)(((uint64_t)r * m) >> 32); }
+
+/* ------------------------------------------------------------------------
+ * Mesh geometry.  x = column, y = row, North = y-1 (R10); non-toroidal (R9).
+ * ---------------------------------------------------------------------- */
+static uint32_t xof(const orc_sim *s, uint32_t n) { return n % s->W; }
+static uint32_t yof(const orc_sim *s, uint32_t n) { return n / s->W; }
+
+static int has_nbr(uint32_t W, uint32_t H, uint32_t n, int d)
+{
+    uint32_t x = n % W, y = n / W;
+    switch (d) {
+    case DIR_N: return y > 0;
+    case DIR_S: return y + 1 < H;
+    case DIR_E: return x + 1 < W;
+    default:    return x > 0;
+    }
+}
+
+static uint32_t nbr(uint32_t W, uint32_t n, int d)
+{
+    switch (d) {
+    case DIR_N: return n - W;
+    case DIR_S: return n + W;
+    case DIR_E: return n + 1;
+    default:    return n - 1;
+    }
+}
+
+static int opp(int d)
+{
+    switch (d) {
+    case DIR_N: return DIR_S;
+    case DIR_S: return DIR_N;
+    case DIR_E: return DIR_W;
+    default:    return DIR_E;
+    }
+}
+
+static int degree(uint32_t W, uint32_t H, uint32_t n)
+{
+    int k = 0;
+    for (int d = 0; d < 4; ++d) k += has_nbr(W, H, n, d);
+    return k;
+}
+
+/* ------------------------------------------------------------------------
+ * Statistics helpers (R31)
+ * ---------------------------------------------------------------------- */
+static void hist_add(const orc_sim *s, uint64_t *h, uint64_t v)
+{
+    uint64_t nb = s->cfg.hist_bins;
+    h[v < nb - 1 ? v : nb - 1] += 1;
+}
+
+/* ------------------------------------------------------------------------
+ * Send FIFO (Core.ToBeSend; bounded, R21)
+ * ---------------------------------------------------------------------- */
+static void enq(orc_sim *s, uint32_t n, uint32_t kind, uint32_t dst, uint32_t payload,
+                uint32_t nfl)
+{
+    Node *c = &s->nodes[n];
+    if (dst == n) fail(s, ORC_EASSERT, "packet addressed to its own node");
+    if (c->count == s->cfg.sendq_cap) {
+        s->c.drops[kind] += 1;
+        return;
+    }
+    Packet *p = &c->fifo[(c->head + c->count) % s->cfg.sendq_cap];
+    p->kind = kind; p->dst = dst; p->payload = payload; p->nfl = nfl;
+    c->count += 1;
+    s->c.packets_enqueued += 1;
+}
+
+/* ------------------------------------------------------------------------
+ * L2 slice: set-associative, LRU with invalid-first and lowest-way ties
+ * ("local victim selection"; R23, R24)
+ * ---------------------------------------------------------------------- */
+static int l2_hit(orc_sim *s, uint32_t n, uint32_t T)
+{
+    uint32_t set = T % s->cfg.l2_sets;
+    Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways];
+    for (uint32_t w = 0; w < s->cfg.l2_ways; ++w) {
+        if (L[w].valid && L[w].tag == T) {
+            L[w].stamp = s->t;
+            return 1;
+        }
+    }
+    return 0;
+}
+
+/* EV handler at home h (R13): the only writer of loc[T] besides DIRSERVICE */
+static void ev_handler(orc_sim *s, uint32_t h, uint32_t T, uint32_t src)
+{
+    (void)h;
+    LocEntry *e = &s->loc[T];
+    if (e->holder != src) fail(s, ORC_EASSERT, "EV from a node that is not the recorded holder");
+    if (e->pend > 0) e->pend -= 1;
+    else e->holder = HOLDER_NONE;
+    s->c.evs_received += 1;
+}
+
+/* Replacement event "when a new cache block comes to L2 cache from main
+ * memory"; the victim's directory entry is deleted by a
+ * message to its home (R13). */
+static void install(orc_sim *s, uint32_t n, uint32_t T)
+{
+    uint32_t set = T % s->cfg.l2_sets;
+    Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways];
+    uint32_t w, victim = 0;
+    int found_invalid = 0;
+    for (w = 0; w < s->cfg.l2_ways; ++w) {
+        if (!L[w].valid) { victim = w; found_invalid = 1; break; }
+    }
+    if (!found_invalid) {
+        victim = 0;
+        for (w = 1; w < s->cfg.l2_ways; ++w)
+            if (L[w].stamp < L[victim].stamp) victim = w;
+    }
+    if (L[victim].valid) {
+        uint32_t V = L[victim].tag;
+        uint32_t hv = V % s->N;
+        s->c.evictions += 1;
+        s->c.evs_sent += 1;
+        if (hv == n) ev_handler(s, n, V, n);
+        else enq(s, n, K_EV, hv, V, 1);
+    }
+    L[victim].valid = 1;
+    L[victim].tag = T;
+    L[victim].stamp = s->t;
+    s->c.installs += 1;
+}
+
+/* An access is complete: record its latency (R31) and free the core */
+static void complete(orc_sim *s, uint32_t n)
+{
+    Node *c = &s->nodes[n];
+    hist_add(s, s->ha, s->t - c->start);
+    s->c.completed += 1;
+    c->mode = M_IDLE;
+}
+
+/* Negative directory reply: fetch from memory, install at the requester
+ * ("new request to next higher level memory"; P:L75 local placement). */
+static void receive_ndr(orc_sim *s, uint32_t n)
+{
+    Node *c = &s->nodes[n];
+    if (c->mode != M_WAIT_DIR) fail(s, ORC_EASSERT, "NDR at a core that is not waiting for the directory");
+    s->c.mem_requests += 1;
+    c->mode = M_MEMWAIT;
+    c->install = 1;
+    c->ready = s->t + s->cfg.mem_lat;
+}
+
+/* Positive directory reply: request the holder (Fig. 4 step 3) */
+static void receive_dr(orc_sim *s, uint32_t n, uint32_t holder)
+{
+    Node *c = &s->nodes[n];
+    if (c->mode != M_WAIT_DIR) fail(s, ORC_EASSERT, "DR at a core that is not waiting for the directory");
+    s->c.requests_made += 1;
+    enq(s, n, K_RQ, holder, c->tag, 1);
+    c->mode = M_WAIT_DATA;
+}
+
+/* Directory lookup at home h for requester r (Fig. 4 steps 1-2; R12-R14, R28) */
+static void dir_service(orc_sim *s, uint32_t h, uint32_t T, uint32_t r)
+{
+    LocEntry *e = &s->loc[T];
+    uint32_t kind, payload;
+    s->c.dir_searches += 1;
+    if (e->holder == HOLDER_NONE) {
+        e->holder = r;                     /* reserve: local placement */
+        kind = K_NDR; payload = T;
+    } else if (e->holder == r) {
+        e->pend += 1;                      /* r's EV of T is still in flight (R13) */
+        if (e->pend > PEND_MAX) fail(s, ORC_EOVERFLOW, "directory pend count overflow");
+        kind = K_NDR; payload = T;
+    } else {
+        kind = K_DR; payload = e->holder;
+    }
+    if (r == h) {                          /* loopback: no flits (R28) */
+        if (kind == K_NDR) receive_ndr(s, r);
+        else receive_dr(s, r, payload);
+    } else {
+        enq(s, h, kind, r, payload, 1);
+    }
+}
+
+/* A new access by the core of n to block T (Phase 1; R19) */
+static void start_access(orc_sim *s, uint32_t n, uint32_t T)
+{
+    Node *c = &s->nodes[n];
+    c->tag = T;
+    c->start = s->t;
+    c->rx = 0;
+    s->c.accesses += 1;
+    if (l2_hit(s, n, T)) {
+        s->c.l2_hits += 1;
+        if (s->cfg.l2_hit_lat == 0) {
+            complete(s, n);
+        } else {
+            c->mode = M_L2WAIT;
+            c->ready = s->t + s->cfg.l2_hit_lat;
+        }
+    } else {
+        uint32_t h = T % s->N;             /* home node of T (R12) */
+        s->c.l2_misses += 1;
+        c->mode = M_WAIT_DIR;
+        if (h == n) dir_service(s, n, T, n);
+        else enq(s, n, K_DA, h, T, 1);
+    }
+}
+
+/* Next script event of node n that is due at cycle t, if any. */
+static int script_next(orc_sim *s, uint32_t n, uint32_t *value)
+{
+    Node *c = &s->nodes[n];
+    if (c->script_pos < c->script_end && s->script[c->script_pos].cycle <= s->t) {
+        *value = s->script[c->script_pos].value;
+        c->script_pos += 1;
+        c->script_used += 1;
+        return 1;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------
+ * Phase 1: the core step.
+ * ---------------------------------------------------------------------- */
+static void phase1(orc_sim *s, uint32_t n)
+{
+    Node *c = &s->nodes[n];
+    uint32_t r[4], v;
+
+    if (s->cfg.mode == ORC_MODE_UR) {
+        /* uniform-random probes, open loop (R26) */
+        if (!s->gen_enabled) return;
+        uint32_t dst;
+        int fire = 0;
+        if (script_next(s, n, &v)) {
+            fire = 1; dst = v;
+        } else {
+            draw(s, n, s->t, r);
+            if (r[0] < s->cfg.thr_inj) {
+                uint32_t d = mulhi(r[1], s->N - 1);
+                if (d >= n) d += 1;          /* skip self */
+                fire = 1; dst = d;
+            }
+        }
+        if (fire) {
+            s->c.generated += 1;
+            enq(s, n, K_PROBE, dst, 0, 1);
+        }
+        return;
+    }
+
+    /* LSPD */
+    if (c->mode == M_L2WAIT && c->ready == s->t) complete(s, n);
+    if (c->mode == M_MEMWAIT && c->ready == s->t) {
+        if (c->install) install(s, n, c->tag);
+        complete(s, n);
+    }
+    if (c->mode == M_IDLE && s->gen_enabled) {
+        uint32_t T;
+        int fire = 0;
+        if (script_next(s, n, &v)) {
+            fire = 1; T = v;
+        } else {
+            draw(s, n, s->t, r);
+            if (r[0] < s->cfg.thr_inj) {
+                uint32_t TPN = s->cfg.tags_per_node, PRIV = s->cfg.priv_tags;
+                fire = 1;
+                if (r[1] < s->cfg.thr_priv)
+                    T = n * TPN + mulhi(r[2], PRIV);                          /* private */
+                else
+                    T = mulhi(r[2], s->N) * TPN + PRIV + mulhi(r[3], TPN - PRIV); /* shared */
+            }
+        }
+        if (fire) start_access(s, n, T);
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * Phase 2: "sort the all incoming flits including injection
+ * flits according to age and assign output port according to their priority.
+ * If there is a conflict it simply deflect to any free port except the
+ * ejection port."
+ * ---------------------------------------------------------------------- */
+typedef struct { uint32_t dst, src; uint64_t age, inj; } ArbFlit;
+
+/* 1 if a ranks strictly before b (R1, R2) */
+static int ranks_before(uint32_t prio, const ArbFlit *a, const ArbFlit *b)
+{
+    if (prio == ORC_PRIO_DEFLECT && a->age != b->age) return a->age > b->age;
+    if (a->inj != b->inj) return a->inj < b->inj;
+    return a->src < b->src;
+}
+
+/* Router decision for flits F[0..nf-1] at node n.  Writes port[i] and
+ * deflected[i].  Returns -1 if nf exceeds the degree. */
+static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t nf,
+                     const ArbFlit *F, int *port, int *deflected)
+{
+    uint32_t order[5];
+    int used[4] = { 0, 0, 0, 0 };
+    int eject_taken = 0;
+    uint32_t x = n % W, y = n / W;
+
+    if ((int)nf > degree(W, H, n)) return -1;
+    /* ranking component: "Priority Sort", insertion sort */
+    for (uint32_t i = 0; i < nf; ++i) {
+        uint32_t j = i;
+        order[i] = i;
+        while (j > 0 && ranks_before(prio, &F[order[j]], &F[order[j - 1]])) {
+            uint32_t tmp = order[j]; order[j] = order[j - 1]; order[j - 1] = tmp;
+            --j;
+        }
+    }
+    /* port-selection component: "considers the flits one by one in the order
+     * of their age ... assigns to each flit the output port with highest
+     * priority that has not yet been assigned" */
+    for (uint32_t k = 0; k < nf; ++k) {
+        uint32_t i = order[k];
+        const ArbFlit *f = &F[i];
+        deflected[i] = 0;
+        if (f->dst == n && !eject_taken) {        /* one eject link X (R6) */
+            port[i] = PORT_EJECT;
+            eject_taken = 1;
+            continue;
+        }
+        if (f->dst != n) {                         /* PMDR: x first, then y (R3) */
+            uint32_t dx = f->dst % W, dy = f->dst / W;
+            int p = -1;
+            if (dx != x) {
+                int xp = dx > x ? DIR_E : DIR_W;
+                if (!used[xp]) p = xp;
+            }
+            if (p < 0 && dy != y) {
+                int yp = dy > y ? DIR_S : DIR_N;
+                if (!used[yp]) p = yp;
+            }
+            if (p >= 0) {
+                used[p] = 1;
+                port[i] = p;
+                continue;
+            }
+        }
+        /* deflection: first free existing port in N,S,E,W (R4, R5) */
+        for (int d = 0; d < 4; ++d) {
+            if (has_nbr(W, H, n, d) && !used[d]) {
+                used[d] = 1;
+                port[i] = d;
+                deflected[i] = 1;
+                break;
+            }
+        }
+    }
+    return 0;
+}
+
+int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio,
+                  uint32_t nf, const uint64_t *flits, int *out_port, uint64_t *out_age)
+{
+    ArbFlit F[5] = {{0, 0, 0, 0}};
+    int defl[5];
+    if (nf > 5) return -1;
+    for (uint32_t i = 0; i < nf; ++i) {
+        F[i].dst = (uint32_t)flits[4 * i + 0];
+        F[i].src = (uint32_t)flits[4 * i + 1];
+        F[i].age = flits[4 * i + 2];
+        F[i].inj = flits[4 * i + 3];
+    }
+    if (arbitrate(mesh_w, mesh_h, node, prio, nf, F, out_port, defl) != 0) return -1;
+    for (uint32_t i = 0; i < nf; ++i) out_age[i] = F[i].age + (uint64_t)defl[i];
+    return 0;
+}
+
+static void phase2(orc_sim *s, uint32_t n)
+{
+    Node *c = &s->nodes[n];
+    Flit F[5];
+    ArbFlit A[5];
+    int port[5], defl[5];
+    uint32_t nf = 0;
+    int deg = degree(s->W, s->H, n);
+
+    for (int d = 0; d < 4; ++d) {
+        if (c->in[d].present) {
+            F[nf++] = c->in[d];
+            c->in[d].present = 0;
+        }
+    }
+    /* injection: one flit per cycle through InFromProc, only if a free input
+     * port exists (R7, R8) */
+    if ((int)nf < deg && c->count > 0) {
+        Packet *p = &c->fifo[c->head];
+        Flit f;
+        f.present = 1;
+        f.dst = p->dst; f.src = n; f.kind = p->kind; f.fid = c->next;
+        f.age = 0;                               /* "Newly injected flits age is set to zero" */
+        f.inj = s->t;
+        f.payload = p->payload;
+        F[nf++] = f;
+        s->c.injected += 1;
+        c->next += 1;
+        if (c->next == p->nfl) {
+            c->head = (c->head + 1) % s->cfg.sendq_cap;
+            c->count -= 1;
+            c->next = 0;
+        }
+    }
+    if (nf == 0) return;
+    for (uint32_t i = 0; i < nf; ++i) {
+        A[i].dst = F[i].dst; A[i].src = F[i].src; A[i].age = F[i].age; A[i].inj = F[i].inj;
+    }
+    if (arbitrate(s->W, s->H, n, s->cfg.prio, nf, A, port, defl) != 0) {
+        fail(s, ORC_EASSERT, "more flits than ports at a router");
+        return;
+    }
+    if (s->debug & ORC_DBG_INVARIANTS) {
+        /* top-priority progress: the rank-1 flit ejects or takes its
+         * first productive port */
+        uint32_t best = 0;
+        for (uint32_t i = 1; i < nf; ++i)
+            if (ranks_before(s->cfg.prio, &A[i], &A[best])) best = i;
+        if (defl[best]) fail(s, ORC_EASSERT, "top-priority flit was deflected");
+        if (A[best].dst != n) {
+            uint32_t x = xof(s, n), y = yof(s, n), dx = A[best].dst % s->W, dy = A[best].dst / s->W;
+            int want = dx != x ? (dx > x ? DIR_E : DIR_W) : (dy > y ? DIR_S : DIR_N);
+            if (port[best] != want) fail(s, ORC_EASSERT, "top-priority flit not on its first productive port");
+        } else if (port[best] != PORT_EJECT) {
+            fail(s, ORC_EASSERT, "top-priority flit at destination not ejected");
+        }
+    }
+    for (uint32_t i = 0; i < nf; ++i) {
+        Flit f = F[i];
+        if (port[i] == PORT_EJECT) {
+            c->has_ej = 1;
+            c->ej = f;
+            continue;
+        }
+        if (defl[i]) {
+            f.age += 1;                           /* "When a flit get deflected its age get incremented" */
+            s->c.deflections += 1;
+            if (f.age > AGE_MAX) fail(s, ORC_EOVERFLOW, "flit age overflow");
+        }
+        if (!has_nbr(s->W, s->H, n, port[i])) {
+            fail(s, ORC_EASSERT, "flit routed off the mesh");
+            continue;
+        }
+        uint32_t m = nbr(s->W, n, port[i]);
+        int slot = opp(port[i]);
+        if (s->nodes[m].nin[slot].present) fail(s, ORC_EASSERT, "two flits on one link");
+        s->nodes[m].nin[slot] = f;
+        s->c.hops += 1;
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * Phase 3: eject, re-assemble, service the
+ * delivered packet (Fig. 4; trap P:L201).
+ * ---------------------------------------------------------------------- */
+static void phase3(orc_sim *s, uint32_t n)
+{
+    Node *c = &s->nodes[n];
+    if (!c->has_ej) return;
+    c->has_ej = 0;
+    Flit f = c->ej;
+    s->c.ejected += 1;
+    hist_add(s, s->hl, s->t - f.inj);
+    hist_add(s, s->hd, f.age);
+    switch (f.kind) {
+    case K_PROBE:
+        s->c.probes_delivered += 1;
+        break;
+    case K_DA:
+        dir_service(s, n, f.payload, f.src);
+        break;
+    case K_DR:
+        receive_dr(s, n, f.payload);
+        break;
+    case K_NDR:
+        receive_ndr(s, n);
+        break;
+    case K_RQ:
+        s->c.requests_received += 1;
+        if (l2_hit(s, n, f.payload)) {
+            s->c.replies_sent += 1;
+            enq(s, n, K_RA, f.src, f.payload, s->cfg.nfl_ra);
+        } else {
+            s->c.traps_sent += 1;                 /* "send the invalid packet" */
+            enq(s, n, K_TRAP, f.src, f.payload, 1);
+        }
+        break;
+    case K_RA:
+        if (c->mode != M_WAIT_DATA) fail(s, ORC_EASSERT, "RA flit at a core not waiting for data");
+        c->rx += 1;
+        if (c->rx == s->cfg.nfl_ra) {
+            c->rx = 0;
+            s->c.replies_received += 1;
+            complete(s, n);
+        }
+        break;
+    case K_TRAP:
+        if (c->mode != M_WAIT_DATA) fail(s, ORC_EASSERT, "TRAP at a core not waiting for data");
+        s->c.traps_received += 1;
+        s->c.mem_requests += 1;
+        c->mode = M_MEMWAIT;
+        c->install = 0;                           /* R16: no install */
+        c->ready = s->t + s->cfg.mem_lat;
+        break;
+    case K_EV:
+        ev_handler(s, n, f.payload, f.src);
+        break;
+    default:
+        fail(s, ORC_EASSERT, "unknown flit kind");
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * Debug invariants (DESIGN 3.5 / SURVEY P2, P3, P9)
+ * ---------------------------------------------------------------------- */
+static void check_invariants(orc_sim *s)
+{
+    int64_t occ = 0;
+    for (uint32_t n = 0; n < s->N; ++n) {
+        int k = 0;
+        for (int d = 0; d < 4; ++d) {
+            if (s->nodes[n].in[d].present) {
+                ++k;
+                if (!has_nbr(s->W, s->H, n, d)) fail(s, ORC_EASSERT, "flit on a missing link");
+            }
+        }
+        if (k > degree(s->W, s->H, n)) fail(s, ORC_EASSERT, "more flits than degree");
+        occ += k;
+    }
+    if (s->c.injected != s->c.ejected + occ) fail(s, ORC_EASSERT, "flit conservation violated");
+    if (s->cfg.mode == ORC_MODE_LSPD) {
+        /* single copy: each T valid in <= 1 slice; holder NONE => pend 0 */
+        uint32_t lines = s->cfg.l2_sets * s->cfg.l2_ways;
+        uint8_t *seen = calloc(s->ntags, 1);
+        if (!seen) return;
+        for (uint32_t n = 0; n < s->N; ++n)
+            for (uint32_t i = 0; i < lines; ++i) {
+                Line *L = &s->nodes[n].l2[i];
+                if (!L->valid) continue;
+                if (seen[L->tag]) fail(s, ORC_EASSERT, "block valid in two slices");
+                seen[L->tag] = 1;
+            }
+        free(seen);
+        for (uint64_t T = 0; T < s->ntags; ++T)
+            if (s->loc[T].holder == HOLDER_NONE && s->loc[T].pend != 0)
+                fail(s, ORC_EASSERT, "pend without holder");
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * One simulated cycle: the serial main loop body.
+ * ---------------------------------------------------------------------- */
+static void cycle(orc_sim *s)
+{
+    uint32_t N = s->N;
+    int rev = (s->debug & ORC_DBG_REVERSE) != 0;
+    for (uint32_t i = 0; i < N; ++i) phase1(s, rev ? N - 1 - i : i);
+    for (uint32_t i = 0; i < N; ++i) phase2(s, rev ? N - 1 - i : i);
+    for (uint32_t i = 0; i < N; ++i) phase3(s, rev ? N - 1 - i : i);
+    /* transfer: outputs of t become the inputs of t+1 (R11) */
+    for (uint32_t n = 0; n < N; ++n) {
+        Node *c = &s->nodes[n];
+        for (int d = 0; d < 4; ++d) {
+            c->in[d] = c->nin[d];
+            c->nin[d].present = 0;
+        }
+    }
+    s->t += 1;
+    s->c.cycle = (int64_t)s->t;
+    if (s->debug & ORC_DBG_INVARIANTS) check_invariants(s);
+}
+
+/* ------------------------------------------------------------------------
+ * Public API
+ * ---------------------------------------------------------------------- */
+static int cmp_event(const void *a, const void *b)
+{
+    const orc_event *x = a, *y = b;
+    if (x->node != y->node) return x->node < y->node ? -1 : 1;
+    if (x->cycle != y->cycle) return x->cycle < y->cycle ? -1 : 1;
+    return 0;
+}
+
+int orc_create(const orc_config *cfg, orc_sim **out)
+{
+    *out = NULL;
+    if (!cfg) { set_err("null config"); return ORC_EINVAL; }
+    uint32_t W = cfg->mesh_w, H = cfg->mesh_h;
+    if (W < 2 || H < 2 || W > 2048 || H > 2048 || (uint64_t)W * H > (1u << 21)) {
+        set_err("mesh must be 2..2048 per side and at most 2^21 nodes"); return ORC_EINVAL;
+    }
+    if (cfg->mode > 1 || cfg->prio > 1) { set_err("bad mode/prio"); return ORC_EINVAL; }
+    if (cfg->sendq_cap == 0 || cfg->sendq_cap > 1024 || (cfg->sendq_cap & (cfg->sendq_cap - 1))) {
+        set_err("sendq_cap must be a power of two in 1..1024"); return ORC_EINVAL;
+    }
+    if (cfg->hist_bins == 0 || cfg->hist_bins > 65536) { set_err("hist_bins must be 1..65536"); return ORC_EINVAL; }
+    if (cfg->nfl_ra < 1 || cfg->nfl_ra > 8) { set_err("nfl_ra must be 1..8"); return ORC_EINVAL; }
+    uint64_t N = (uint64_t)W * H;
+    if (cfg->mode == ORC_MODE_LSPD) {
+        if (cfg->l2_sets < 1 || cfg->l2_sets > 65536 || cfg->l2_ways < 1 || cfg->l2_ways > 16) {
+            set_err("l2 geometry out of range"); return ORC_EINVAL;
+        }
+        if (cfg->tags_per_node < 2 || cfg->priv_tags < 1 || cfg->priv_tags >= cfg->tags_per_node) {
+            set_err("need 1 <= priv_tags < tags_per_node"); return ORC_EINVAL;
+        }
+        if ((uint64_t)cfg->tags_per_node * N > (1ull << 31)) { set_err("tag space exceeds 2^31"); return ORC_EINVAL; }
+        if (cfg->mem_lat < 1 || cfg->mem_lat >= (1u << 30) || cfg->l2_hit_lat >= (1u << 30)) {
+            set_err("latency out of range"); return ORC_EINVAL;
+        }
+    }
+    for (uint64_t i = 0; i < cfg->n_script; ++i) {
+        const orc_event *e = &cfg->script[i];
+        if (e->node >= N) { set_err("script node out of range"); return ORC_EINVAL; }
+        if (cfg->mode == ORC_MODE_UR && (e->value >= N || e->value == e->node)) {
+            set_err("script probe destination invalid"); return ORC_EINVAL;
+        }
+        if (cfg->mode == ORC_MODE_LSPD && (uint64_t)e->value >= (uint64_t)cfg->tags_per_node * N) {
+            set_err("script tag out of range"); return ORC_EINVAL;
+        }
+    }
+
+    orc_sim *s = calloc(1, sizeof *s);
+    if (!s) { set_err("out of memory"); return ORC_ENOMEM; }
+    s->cfg = *cfg;
+    s->W = W; s->H = H; s->N = (uint32_t)N;
+    s->gen_enabled = 1;
+    s->nodes = calloc(N, sizeof(Node));
+    s->fifo_store = calloc(N * cfg->sendq_cap, sizeof(Packet));
+    s->hl = calloc(cfg->hist_bins, sizeof(uint64_t));
+    s->hd = calloc(cfg->hist_bins, sizeof(uint64_t));
+    s->ha = calloc(cfg->hist_bins, sizeof(uint64_t));
+    int bad = !s->nodes || !s->fifo_store || !s->hl || !s->hd || !s->ha;
+    if (cfg->mode == ORC_MODE_LSPD && !bad) {
+        uint64_t lines = (uint64_t)cfg->l2_sets * cfg->l2_ways;
+        s->ntags = (uint64_t)cfg->tags_per_node * N;
+        s->l2_store = calloc(N * lines, sizeof(Line));
+        s->loc = malloc(s->ntags * sizeof(LocEntry));
+        bad = !s->l2_store || !s->loc;
+        if (!bad) {
+            for (uint64_t T = 0; T < s->ntags; ++T) { s->loc[T].holder = HOLDER_NONE; s->loc[T].pend = 0; }
+            for (uint64_t n = 0; n < N; ++n) s->nodes[n].l2 = &s->l2_store[n * lines];
+        }
+    }
+    if (cfg->n_script && !bad) {
+        s->script = malloc(cfg->n_script * sizeof(orc_event));
+        bad = !s->script;
+        if (!bad) {
+            memcpy(s->script, cfg->script, cfg->n_script * sizeof(orc_event));
+            /* stable order per node: (node, cycle), ties keep input order */
+            for (uint64_t i = 1; i < cfg->n_script; ++i) {      /* insertion sort: stable */
+                orc_event e = s->script[i];
+                uint64_t j = i;
+                while (j > 0 && cmp_event(&e, &s->script[j - 1]) < 0) { s->script[j] = s->script[j - 1]; --j; }
+                s->script[j] = e;
+            }
+        }
+    }
+    s->cfg.script = NULL;
+    if (bad) { orc_destroy(s); set_err("out of memory"); return ORC_ENOMEM; }
+    for (uint64_t n = 0; n < N; ++n) {
+        s->nodes[n].fifo = &s->fifo_store[n * cfg->sendq_cap];
+        s->nodes[n].mode = M_IDLE;
+    }
+    {
+        uint64_t i = 0;
+        for (uint64_t n = 0; n < N; ++n) {
+            s->nodes[n].script_pos = i;
+            while (i < cfg->n_script && s->script[i].node == n) ++i;
+            s->nodes[n].script_end = i;
+        }
+    }
+    *out = s;
+    return ORC_OK;
+}
+
+void orc_destroy(orc_sim *s)
+{
+    if (!s) return;
+    free(s->nodes); free(s->fifo_store); free(s->l2_store); free(s->loc);
+    free(s->script); free(s->hl); free(s->hd); free(s->ha);
+    free(s);
+}
+
+int orc_set_debug(orc_sim *s, int flags) { s->debug = flags; return ORC_OK; }
+
+int orc_run(orc_sim *s, uint64_t n_cycles)
+{
+    if (s->err) return s->err;
+    for (uint64_t i = 0; i < n_cycles && !s->err; ++i) cycle(s);
+    return s->err;
+}
+
+static int quiescent(const orc_sim *s)
+{
+    for (uint32_t n = 0; n < s->N; ++n) {
+        const Node *c = &s->nodes[n];
+        if (c->count || c->mode != M_IDLE) return 0;
+        for (int d = 0; d < 4; ++d) if (c->in[d].present) return 0;
+    }
+    return 1;
+}
+
+/* run with generation disabled until quiescent (R30) */
+int orc_drain(orc_sim *s, uint64_t max_cycles, uint64_t *used, int *drained)
+{
+    uint64_t k = 0;
+    int q;
+    if (s->err) return s->err;
+    s->gen_enabled = 0;
+    while (!(q = quiescent(s)) && k < max_cycles && !s->err) { cycle(s); ++k; }
+    s->gen_enabled = 1;
+    if (used) *used = k;
+    if (drained) *drained = q;
+    return s->err;
+}
+
+int orc_stats(const orc_sim *s, orc_counters *out, uint64_t *hl, uint64_t *hd, uint64_t *ha,
+              uint32_t nbins)
+{
+    if (out) *out = s->c;
+    if (hl || hd || ha) {
+        if (nbins != s->cfg.hist_bins) { set_err("nbins mismatch"); return ORC_EINVAL; }
+        if (hl) memcpy(hl, s->hl, nbins * sizeof(uint64_t));
+        if (hd) memcpy(hd, s->hd, nbins * sizeof(uint64_t));
+        if (ha) memcpy(ha, s->ha, nbins * sizeof(uint64_t));
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * Canonical state hash (DESIGN 3.7): sum over (domain, index, tuple) of
+ * mix(mix(dom<<56 ^ index) ^ tuplehash) mod 2^64.
+ * ---------------------------------------------------------------------- */
+static uint64_t mix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+static uint64_t tuple_hash(const uint64_t *v, int k)
+{
+    uint64_t h = (uint64_t)k;
+    for (int i = 0; i < k; ++i) h = mix64(h ^ v[i]);
+    return h;
+}
+
+static uint64_t term(uint64_t dom, uint64_t idx, const uint64_t *v, int k)
+{
+    return mix64(mix64((dom << 56) ^ idx) ^ tuple_hash(v, k));
+}
+
+enum { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, D_LOC = 6,
+       D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10 };
+
+uint64_t orc_state_hash(const orc_sim *s)
+{
+    uint64_t H = 0, v[8];
+    for (uint32_t n = 0; n < s->N; ++n) {
+        const Node *c = &s->nodes[n];
+        for (int d = 0; d < 4; ++d) {
+            const Flit *f = &c->in[d];
+            if (!f->present) continue;
+            v[0] = f->dst; v[1] = f->src; v[2] = f->kind; v[3] = f->fid;
+            v[4] = f->payload; v[5] = f->age; v[6] = f->inj;
+            H += term(D_LINK, (uint64_t)n * 4 + d, v, 7);
+        }
+        for (uint32_t k = 0; k < c->count; ++k) {
+            const Packet *p = &c->fifo[(c->head + k) % s->cfg.sendq_cap];
+            v[0] = p->kind; v[1] = p->dst; v[2] = p->payload; v[3] = p->nfl;
+            H += term(D_FIFO, ((uint64_t)n << 16) + k, v, 4);
+        }
+        if (c->next) { v[0] = c->next; H += term(D_FIFONEXT, n, v, 1); }
+        if (c->mode != M_IDLE) {
+            uint64_t ready = 0, tag = 0, inst = 0, start = c->start, rx = 0;
+            switch (c->mode) {
+            case M_L2WAIT:    ready = c->ready; break;
+            case M_WAIT_DIR:  tag = c->tag; break;
+            case M_WAIT_DATA: tag = c->tag; rx = c->rx; break;
+            case M_MEMWAIT:   ready = c->ready; tag = c->tag; inst = (uint64_t)c->install; break;
+            }
+            v[0] = (uint64_t)c->mode; v[1] = ready; v[2] = tag; v[3] = inst; v[4] = start; v[5] = rx;
+            H += term(D_CORE, n, v, 6);
+        }
+        if (s->cfg.mode == ORC_MODE_LSPD) {
+            uint32_t S = s->cfg.l2_sets, Wy = s->cfg.l2_ways;
+            for (uint32_t st = 0; st < S; ++st)
+                for (uint32_t w = 0; w < Wy; ++w) {
+                    const Line *L = &c->l2[(uint64_t)st * Wy + w];
+                    if (!L->valid) continue;
+                    v[0] = L->tag; v[1] = L->stamp;
+                    H += term(D_L2, ((uint64_t)n * S + st) * Wy + w, v, 2);
+                }
+        }
+        if (c->script_used) { v[0] = c->script_used; H += term(D_SCRIPT, n, v, 1); }
+    }
+    for (uint64_t T = 0; T < s->ntags; ++T) {
+        const LocEntry *e = &s->loc[T];
+        if (e->holder == HOLDER_NONE && e->pend == 0) continue;
+        v[0] = e->holder == HOLDER_NONE ? 0 : (uint64_t)e->holder + 1;
+        v[1] = e->pend;
+        H += term(D_LOC, T, v, 2);
+    }
+    {
+        const int64_t *cnt = &s->c.generated;      /* generated .. drops[7] */
+        int ncnt = (int)((sizeof(orc_counters) - sizeof(int64_t)) / sizeof(int64_t));
+        for (int i = 0; i < ncnt; ++i) { v[0] = (uint64_t)cnt[i]; H += term(D_CNT, (uint64_t)i, v, 1); }
+    }
+    {
+        const uint64_t *hs[3] = { s->hl, s->hd, s->ha };
+        for (int h = 0; h < 3; ++h)
+            for (uint32_t b = 0; b < s->cfg.hist_bins; ++b)
+                if (hs[h][b]) { v[0] = hs[h][b]; H += term(D_HIST, ((uint64_t)h << 32) + b, v, 1); }
+    }
+    v[0] = s->t;
+    H += term(D_CYCLE, 0, v, 1);
+    return H;
+}
+
+/* ------------------------------------------------------------------------
+ * Test peeks
+ * ---------------------------------------------------------------------- */
+int64_t orc_links_occupied(const orc_sim *s, int64_t *age_sum)
+{
+    int64_t k = 0, a = 0;
+    for (uint32_t n = 0; n < s->N; ++n)
+        for (int d = 0; d < 4; ++d)
+            if (s->nodes[n].in[d].present) { ++k; a += (int64_t)s->nodes[n].in[d].age; }
+    if (age_sum) *age_sum = a;
+    return k;
+}
+
+int64_t orc_fifo_packets(const orc_sim *s)
+{
+    int64_t k = 0;
+    for (uint32_t n = 0; n < s->N; ++n) k += s->nodes[n].count;
+    return k;
+}
+
+int64_t orc_cores_busy(const orc_sim *s)
+{
+    int64_t k = 0;
+    for (uint32_t n = 0; n < s->N; ++n) k += s->nodes[n].mode != M_IDLE;
+    return k;
+}
+
+int orc_check_directory_quiescent(const orc_sim *s)
+{
+    if (s->cfg.mode != ORC_MODE_LSPD) return 0;
+    uint32_t lines = s->cfg.l2_sets * s->cfg.l2_ways;
+    uint32_t *holder = malloc(s->ntags * sizeof(uint32_t));
+    if (!holder) return -2;
+    for (uint64_t T = 0; T < s->ntags; ++T) holder[T] = HOLDER_NONE;
+    int bad = 0;
+    for (uint32_t n = 0; n < s->N; ++n)
+        for (uint32_t i = 0; i < lines; ++i) {
+            const Line *L = &s->nodes[n].l2[i];
+            if (!L->valid) continue;
+            if (holder[L->tag] != HOLDER_NONE) bad = 1;
+            holder[L->tag] = n;
+        }
+    for (uint64_t T = 0; T < s->ntags && !bad; ++T) {
+        if (s->loc[T].holder != holder[T] || s->loc[T].pend != 0) bad = 1;
+    }
+    free(holder);
+    return bad ? -1 : 0;
+}
+
+int orc_core(const orc_sim *s, uint32_t n, uint64_t out[6])
+{
+    if (n >= s->N) return ORC_EINVAL;
+    const Node *c = &s->nodes[n];
+    out[0] = (uint64_t)c->mode; out[1] = c->ready; out[2] = c->tag;
+    out[3] = (uint64_t)c->install; out[4] = c->start; out[5] = c->rx;
+    return ORC_OK;
+}
+
+int orc_l2_line(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint64_t out[3])
+{
+    if (s->cfg.mode != ORC_MODE_LSPD || n >= s->N || set >= s->cfg.l2_sets || way >= s->cfg.l2_ways)
+        return ORC_EINVAL;
+    const Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways + way];
+    out[0] = (uint64_t)L->valid; out[1] = L->tag; out[2] = L->stamp;
+    return ORC_OK;
+}
+
+int orc_loc(const orc_sim *s, uint32_t T, uint64_t out[2])
+{
+    if (T >= s->ntags) return ORC_EINVAL;
+    out[0] = s->loc[T].holder; out[1] = s->loc[T].pend;
+    return ORC_OK;
+}

@@ -1,0 +1,120 @@
+/*
+ * noc_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Interface of the plain, slow, single-threaded CPU oracle of the
+ * bufferless-NoC + LSPD-L2 cycle simulation of Kumar & Sahu,
+ * arXiv 1508.03235 ("Bufferless NOC Simulation of Large Multicore System on
+ * GPU Hardware").  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or helper with the CUDA product library
+ * (paper_1508_03235_b200/csrc, include/noc_sim.h).
+ *
+ * Citations: "P:Lnn" = PAPER.md line nn; readings R1..R35 are listed in
+ * DESIGN.md section 3 (they follow SURVEY.md section 8(c.3)).
+ */
+#ifndef NOC_ORACLE_H
+#define NOC_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_OK         0
+#define ORC_EINVAL    -1
+#define ORC_ENOMEM    -2
+#define ORC_EOVERFLOW -5
+#define ORC_EASSERT   -7   /* a debug invariant failed (see orc_last_error) */
+
+/* traffic modes (R35) */
+#define ORC_MODE_UR   0    /* uniform-random 1-flit probes, open loop       */
+#define ORC_MODE_LSPD 1    /* core accesses to the LSPD L2 (Fig. 4)  */
+/* priority (R1) */
+#define ORC_PRIO_DEFLECT 0 /* age = #deflections       */
+#define ORC_PRIO_OLDEST  1 /* oldest injection cycle first         */
+
+/* debug flags for orc_set_debug */
+#define ORC_DBG_REVERSE    1  /* iterate nodes in reverse order in every phase */
+#define ORC_DBG_INVARIANTS 2  /* check conservation / exclusivity / directory
+                                 single-copy / top-priority progress per cycle */
+
+typedef struct {
+    uint64_t cycle;   /* earliest cycle the event may be consumed          */
+    uint32_t node;    /* node id y*W+x                                     */
+    uint32_t value;   /* UR: probe destination node; LSPD: block tag T     */
+} orc_event;
+
+typedef struct {
+    uint32_t mesh_w, mesh_h;     /* 2..2048 each, W*H <= 2^21               */
+    uint32_t mode, prio;
+    uint32_t l2_sets, l2_ways;   /* LSPD slice geometry (Table III)         */
+    uint32_t tags_per_node;      /* TPN: tag space = TPN * N                */
+    uint32_t priv_tags;          /* PRIV: private window per node, < TPN    */
+    uint32_t thr_inj;            /* floor(lambda * 2^32)                    */
+    uint32_t thr_priv;           /* floor(p_priv * 2^32)                    */
+    uint32_t l2_hit_lat;         /* >= 0                                    */
+    uint32_t mem_lat;            /* >= 1                                    */
+    uint32_t nfl_ra;             /* flits of the RA data reply, Table I: 4  */
+    uint32_t sendq_cap;          /* packets per send FIFO, power of two     */
+    uint32_t hist_bins;          /* NB, last bin = overflow                 */
+    uint64_t seed;
+    const orc_event *script;     /* optional, may be NULL                   */
+    uint64_t n_script;
+} orc_config;
+
+/* counters, in the order of DESIGN.md section 3.6 */
+typedef struct {
+    int64_t cycle;
+    int64_t generated, packets_enqueued, injected, ejected, hops, deflections;
+    int64_t probes_delivered, accesses, completed, l2_hits, l2_misses;
+    int64_t dir_searches, requests_made, requests_received, replies_sent;
+    int64_t replies_received, traps_sent, traps_received, mem_requests;
+    int64_t installs, evictions, evs_sent, evs_received;
+    int64_t drops[8];
+} orc_counters;
+
+typedef struct orc_sim orc_sim;
+
+int  orc_create(const orc_config *cfg, orc_sim **out);
+void orc_destroy(orc_sim *s);
+int  orc_set_debug(orc_sim *s, int flags);
+int  orc_run(orc_sim *s, uint64_t n_cycles);
+int  orc_drain(orc_sim *s, uint64_t max_cycles, uint64_t *used, int *drained);
+int  orc_stats(const orc_sim *s, orc_counters *out, uint64_t *hist_lat,
+               uint64_t *hist_defl, uint64_t *hist_acc, uint32_t nbins);
+uint64_t orc_state_hash(const orc_sim *s);
+const char *orc_last_error(void);
+
+/* ---- test hooks ------------------------------------------------------ */
+/* Philox4x32-10 with key {k0,k1} on counter c[4] -> out[4]. */
+void orc_philox(uint32_t k0, uint32_t k1, const uint32_t c[4], uint32_t out[4]);
+
+/* One router's stage-2 decision in isolation.
+ *   flits: nf records of 4 u64 {dst, src, age, inj}
+ *   out_port[i]: 0..3 = N,S,E,W output, 4 = eject
+ *   out_age[i] : age after the decision
+ * Returns 0, or -1 if nf > degree. */
+int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio,
+                  uint32_t nf, const uint64_t *flits, int *out_port,
+                  uint64_t *out_age);
+
+/* In-flight flits on links (inputs of the next cycle) and their age sum. */
+int64_t orc_links_occupied(const orc_sim *s, int64_t *age_sum);
+/* Packets waiting in send FIFOs (all nodes). */
+int64_t orc_fifo_packets(const orc_sim *s);
+/* Number of cores not IDLE. */
+int64_t orc_cores_busy(const orc_sim *s);
+/* Directory agreement at quiescence (DESIGN 3.5): 0 if it holds. */
+int  orc_check_directory_quiescent(const orc_sim *s);
+/* Core record of node n: mode, ready, tag, install, start, rx. */
+int  orc_core(const orc_sim *s, uint32_t n, uint64_t out[6]);
+/* L2 slice line (n, set, way): valid, tag, stamp. */
+int  orc_l2_line(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way,
+                 uint64_t out[3]);
+/* Directory entry of tag T: holder (UINT32_MAX = none) and pend. */
+int  orc_loc(const orc_sim *s, uint32_t T, uint64_t out[2]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
