@@ -1,0 +1,170 @@
+// common.cuh -- device-side definitions shared by the kernels of libnocsim.so.
+//
+// Model: DESIGN.md section 3 (Kumar & Sahu, arXiv 1508.03235).  This file is
+// part of the product path; it shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace noc {
+
+// ports / input slots in the paper's order N, S, E, W; 4 = eject
+enum : uint32_t { PN = 0, PS = 1, PE = 2, PW = 3, PX = 4 };
+// message kinds (Table I; DESIGN 3.2)
+enum : uint32_t { KPROBE = 0, KDA = 1, KDR = 2, KNDR = 3, KRQ = 4, KRA = 5, KTRAP = 6, KEV = 7 };
+// core modes (DESIGN 3.2)
+enum : uint32_t { MIDLE = 0, ML2WAIT = 1, MWAITDIR = 2, MWAITDATA = 3, MMEMWAIT = 4 };
+// counter indices (DESIGN 3.6)
+enum : uint32_t {
+    C_GENERATED = 0, C_ENQ, C_INJECTED, C_EJECTED, C_HOPS, C_DEFL, C_PROBES, C_ACCESSES,
+    C_COMPLETED, C_L2HIT, C_L2MISS, C_DIRSEARCH, C_REQMADE, C_REQRCVD, C_REPSENT, C_REPRCVD,
+    C_TRAPSENT, C_TRAPRCVD, C_MEMREQ, C_INSTALLS, C_EVICTIONS, C_EVSENT, C_EVRCVD,
+    C_DROPS = 23, NCOUNTERS = 31
+};
+// error flags
+enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8 };
+
+constexpr uint32_t AGE_MAX = 65535u;   // R32
+constexpr uint32_t PEND_MAX = 1023u;   // R32
+constexpr uint32_t HOLDER_BITS = 22;   // loc entry = (holder+1) | pend << 22   (R36: 4 B)
+constexpr uint32_t HOLDER_MASK = (1u << HOLDER_BITS) - 1u;
+constexpr uint32_t NODE_MASK = (1u << 21) - 1u;
+
+// ---------------------------------------------------------------------------
+// Flit: one 16-byte record (uint4), moved with one 128-bit load/store.
+//   x = dst[0:21) | kind[21:24) | fid[24:27) | age_hi5[27:32)
+//   y = src[0:21) | age_lo11[21:32)
+//   z = injection cycle mod 2^32
+//   w = payload (tag T or holder node)
+// ---------------------------------------------------------------------------
+struct Flit {
+    uint32_t x, y, z, w;
+};
+
+__host__ __device__ __forceinline__ uint32_t f_dst(const Flit &f) { return f.x & NODE_MASK; }
+__host__ __device__ __forceinline__ uint32_t f_kind(const Flit &f) { return (f.x >> 21) & 7u; }
+__host__ __device__ __forceinline__ uint32_t f_fid(const Flit &f) { return (f.x >> 24) & 7u; }
+__host__ __device__ __forceinline__ uint32_t f_src(const Flit &f) { return f.y & NODE_MASK; }
+__host__ __device__ __forceinline__ uint32_t f_age(const Flit &f) { return (f.x >> 27) << 11 | (f.y >> 21); }
+__host__ __device__ __forceinline__ void f_set_age(Flit &f, uint32_t a)
+{
+    f.x = (f.x & 0x07FFFFFFu) | ((a >> 11) << 27);
+    f.y = (f.y & NODE_MASK) | ((a & 0x7FFu) << 21);
+}
+__host__ __device__ __forceinline__ Flit f_make(uint32_t dst, uint32_t kind, uint32_t fid, uint32_t src,
+                                               uint32_t inj, uint32_t payload)
+{
+    Flit f;
+    f.x = dst | (kind << 21) | (fid << 24);
+    f.y = src;
+    f.z = inj;
+    f.w = payload;
+    return f;
+}
+
+// FIFO packet: uint2 {dst[0:21) | kind[21:24) | nfl[24:28), payload}
+// FIFO control word: head[0:10) | count[10:21) | next[21:24)
+__host__ __device__ __forceinline__ uint32_t q_head(uint32_t c) { return c & 1023u; }
+__host__ __device__ __forceinline__ uint32_t q_count(uint32_t c) { return (c >> 10) & 2047u; }
+__host__ __device__ __forceinline__ uint32_t q_next(uint32_t c) { return c >> 21; }
+__host__ __device__ __forceinline__ uint32_t q_make(uint32_t h, uint32_t n, uint32_t nx)
+{
+    return h | (n << 10) | (nx << 21);
+}
+
+// core hot word: mode[29:32) | ready mod 2^29 ; cold record: {start_lo, start_hi, tag, install | rx<<1}
+__host__ __device__ __forceinline__ uint32_t core_mode(uint32_t hot) { return hot >> 29; }
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11, Random123 constants); R25.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ void philox4x32_10(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1,
+                                                      uint32_t c2, uint32_t c3, uint32_t r[4])
+{
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+#ifdef __CUDA_ARCH__
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+#else
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    r[0] = c0; r[1] = c1; r[2] = c2; r[3] = c3;
+}
+
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t r, uint32_t m)
+{
+#ifdef __CUDA_ARCH__
+    return __umulhi(r, m);
+#else
+    return (uint32_t)(((uint64_t)r * m) >> 32);
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Canonical hash (DESIGN 3.7)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+struct TupleHash {
+    uint64_t h;
+    __host__ __device__ explicit TupleHash(int k) : h((uint64_t)k) {}
+    __host__ __device__ TupleHash &add(uint64_t v) { h = mix64(h ^ v); return *this; }
+};
+
+__host__ __device__ __forceinline__ uint64_t hterm(uint64_t dom, uint64_t idx, uint64_t tup)
+{
+    return mix64(mix64((dom << 56) ^ idx) ^ tup);
+}
+
+enum : uint64_t { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, D_LOC = 6,
+                  D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10 };
+
+// ---------------------------------------------------------------------------
+// Device view of one simulation (passed by value to every kernel).
+// All arrays are indexed by the LOCAL node index l in [0, nloc) of this rank's
+// band (rows [row0, row0+rows) of the mesh): global id n = n0 + l.
+// ---------------------------------------------------------------------------
+struct Dev {
+    // geometry and model parameters
+    uint32_t W, H, N, n0, nloc, row0, rows;
+    uint32_t mode, prio, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
+    uint32_t qcap, nb, seed_lo, seed_hi;
+    uint32_t gen;                     // generation enabled (0 during drain)
+    uint32_t has_script;
+    // state
+    uint4 *flit[2];                   // [2][4][nloc] links, slot d of node l
+    uint32_t *flag[2];                // [2][nloc] byte d = stamp of slot d
+    uint32_t *core_hot;               // [nloc]
+    uint4 *core_cold;                 // [nloc]
+    uint32_t *fifo_ctl;               // [nloc]
+    uint2 *fifo_pkt;                  // [nloc][qcap]
+    uint4 *l2;                        // [nloc][sets][ways] {tag+1 (0 = invalid), stamp_lo, stamp_hi, 0}
+    uint32_t *loc;                    // [tpn][nloc] directory entries of tags homed in this band
+    const uint4 *script;              // [n_script] {cycle_lo, cycle_hi, value, 0} grouped by node
+    const uint32_t *script_off;       // [nloc+1]
+    uint32_t *script_pos;             // [nloc] events consumed
+    unsigned long long *cnt;          // [NCOUNTERS]
+    unsigned long long *hist;         // [3][nb]
+    uint32_t *err;                    // [1] error flags
+    // halo (multi-GPU row bands; null when the band is the whole mesh)
+    uint4 *halo_out_flit[2];          // [2 sides][W] flits leaving the band (0 = north, 1 = south)
+    uint32_t *halo_out_flag[2];       // [2 sides][W] stamps
+};
+
+__host__ __device__ __forceinline__ uint8_t stamp_of(uint64_t cycle) { return (uint8_t)(0x80u | (cycle & 0x7Fu)); }
+
+}  // namespace noc

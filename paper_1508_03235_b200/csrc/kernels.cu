@@ -1,0 +1,313 @@
+// kernels.cu -- the CUDA kernels of libnocsim.so (sm_100a) and their launch
+// wrappers.  DESIGN.md section 6 describes the engines:
+//   STEP    : one fused node-step launch per simulated cycle (all three phases
+//             of the paper's loop, in ONE kernel);
+//   PERSIST : one cooperative launch advances many cycles; each CTA owns a
+//             contiguous range of nodes and, between cycles, waits only for the
+//             CTAs whose nodes neighbour its own (neighbour-progress flags,
+//             no grid-wide barrier, no host round trip).
+#include "node_logic.cuh"
+#include "kernels.h"
+
+#include <cooperative_groups.h>
+
+namespace noc {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Flush per-thread register accumulators: warp reduce, then one atomic per warp.
+__device__ __forceinline__ void flush_acc(const Dev &S, const Acc &a, unsigned int *scnt)
+{
+    uint32_t v[4] = {a.injected, a.ejected, a.hops, a.defl};
+    const uint32_t idx[4] = {C_INJECTED, C_EJECTED, C_HOPS, C_DEFL};
+    unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t s = __reduce_add_sync(0xFFFFFFFFu, v[i]);
+        if (lane == 0 && s) {
+            if (scnt) atomicAdd(&scnt[idx[i]], s);
+            else atomicAdd(&S.cnt[idx[i]], (unsigned long long)s);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ init
+__global__ void k_init_loc_nop() {}
+
+// ------------------------------------------------------------------ STEP engine
+template <uint32_t MODE>
+__global__ void __launch_bounds__(256) k_step(Dev S, uint64_t t, uint32_t *activity)
+{
+    uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    Acc acc = {0, 0, 0, 0};
+    Sink K{nullptr, nullptr};
+    bool busy = false;
+    if (l < S.nloc) busy = node_step_global<MODE>(S, K, l, t, acc);
+    flush_acc(S, acc, nullptr);
+    if (activity) {
+        if (__syncthreads_or(busy) && threadIdx.x == 0) atomicAdd(activity, 1u);
+    }
+}
+
+// ------------------------------------------------------------------ PERSIST engine
+// Dynamic shared memory: NCOUNTERS u32 counters, then (optionally) 3*nb u32 bins.
+template <uint32_t MODE>
+__global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, uint32_t ncyc, uint32_t *progress,
+                                                         uint32_t pbase, uint32_t nodes_per_cta, uint32_t smem_hist,
+                                                         uint32_t *activity)
+{
+    extern __shared__ unsigned int sm[];
+    unsigned int *scnt = sm;
+    unsigned int *shist = smem_hist ? sm + NCOUNTERS : nullptr;
+    const uint32_t nsm = NCOUNTERS + (smem_hist ? 3u * S.nb : 0u);
+    for (uint32_t i = threadIdx.x; i < nsm; i += blockDim.x) sm[i] = 0u;
+    __syncthreads();
+
+    const uint32_t G = gridDim.x, b = blockIdx.x;
+    const uint32_t lo_node = b * nodes_per_cta;
+    const uint32_t hi_node = min(S.nloc, lo_node + nodes_per_cta);
+    // CTAs owning nodes within one row (W) of ours: they feed our input links
+    const uint32_t first = lo_node >= S.W ? (lo_node - S.W) / nodes_per_cta : 0u;
+    const uint32_t lastn = min(S.nloc - 1u, hi_node - 1u + S.W);
+    const uint32_t last = min(G - 1u, lastn / nodes_per_cta);
+    Sink K{scnt, shist};
+    Acc acc = {0, 0, 0, 0};
+    __shared__ int s_abort;
+    if (threadIdx.x == 0) s_abort = 0;
+    __syncthreads();
+
+    for (uint32_t c = 0; c < ncyc; ++c) {
+        const uint64_t t = t0 + c;
+        if (c > 0) {
+            // wait until every neighbouring CTA completed cycle t-1
+            const uint32_t target = pbase + c;
+            for (uint32_t j = first + threadIdx.x; j <= last; j += blockDim.x) {
+                if (j == b) continue;
+                uint32_t spins = 0;
+                while ((int32_t)(ld_acquire_u32(&progress[j]) - target) < 0) {
+                    if (++spins > (1u << 24)) {   // a hung neighbour: abort the launch, report
+                        atomicOr(S.err, 0x80000000u);
+                        s_abort = 1;
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            if (s_abort) break;
+        }
+        bool busy = false;
+        for (uint32_t l = lo_node + threadIdx.x; l < hi_node; l += blockDim.x)
+            busy |= node_step_global<MODE>(S, K, l, t, acc);
+        if (activity) {
+            if (__syncthreads_or(busy) && threadIdx.x == 0) atomicAdd(&activity[c], 1u);
+        } else {
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_u32(&progress[b], pbase + c + 1u);
+        }
+    }
+    flush_acc(S, acc, scnt);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < NCOUNTERS; i += blockDim.x)
+        if (scnt[i]) atomicAdd(&S.cnt[i], (unsigned long long)scnt[i]);
+    if (smem_hist)
+        for (uint32_t i = threadIdx.x; i < 3u * S.nb; i += blockDim.x)
+            if (shist[i]) atomicAdd(&S.hist[i], (unsigned long long)shist[i]);
+}
+
+// ------------------------------------------------------------------ drain helper
+__global__ void k_busy_count(Dev S, uint64_t t, uint32_t *out)
+{
+    uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    bool busy = false;
+    if (l < S.nloc) {
+        uint32_t fl = S.flag[(uint32_t)t & 1u][l];
+        uint8_t st = stamp_of(t);
+        for (int d = 0; d < 4; ++d) busy |= ((fl >> (8 * d)) & 0xFFu) == st;
+        busy |= q_count(S.fifo_ctl[l]) > 0;
+        if (S.mode == 1u) busy |= core_mode(S.core_hot[l]) != MIDLE;
+    }
+    if (__syncthreads_or(busy) && threadIdx.x == 0) atomicAdd(out, 1u);
+}
+
+// ------------------------------------------------------------------ state hash
+// Node-owned terms (LINK, FIFO, FIFONEXT, CORE, L2, SCRIPT) of DESIGN 3.7.
+__global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
+{
+    uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t H = 0;
+    if (l < S.nloc) {
+        const uint64_t n = S.n0 + l;
+        const uint32_t b = (uint32_t)t & 1u;
+        const uint8_t st = stamp_of(t);
+        uint32_t fl = S.flag[b][l];
+        for (uint32_t d = 0; d < 4; ++d) {
+            if (((fl >> (8u * d)) & 0xFFu) != st) continue;
+            uint4 v = S.flit[b][(size_t)d * S.nloc + l];
+            Flit f{v.x, v.y, v.z, v.w};
+            uint64_t life = (uint32_t)((uint32_t)t - f.z);
+            uint64_t inj = t - life;
+            TupleHash th(7);
+            th.add(f_dst(f)).add(f_src(f)).add(f_kind(f)).add(f_fid(f)).add(f.w).add(f_age(f)).add(inj);
+            H += hterm(D_LINK, n * 4 + d, th.h);
+        }
+        uint32_t q = S.fifo_ctl[l];
+        for (uint32_t k = 0; k < q_count(q); ++k) {
+            uint2 p = S.fifo_pkt[(size_t)l * S.qcap + ((q_head(q) + k) & (S.qcap - 1u))];
+            TupleHash th(4);
+            th.add((p.x >> 21) & 7u).add(p.x & NODE_MASK).add(p.y).add((p.x >> 24) & 15u);
+            H += hterm(D_FIFO, (n << 16) + k, th.h);
+        }
+        if (q_next(q)) H += hterm(D_FIFONEXT, n, TupleHash(1).add(q_next(q)).h);
+        if (S.mode == 1u) {
+            uint32_t hot = S.core_hot[l];
+            uint32_t mode = core_mode(hot);
+            if (mode != MIDLE) {
+                uint4 cold = S.core_cold[l];
+                uint64_t ready = 0, tag = 0, inst = 0, rx = 0;
+                uint64_t start = ((uint64_t)cold.y << 32) | cold.x;
+                uint64_t r29 = t + (uint64_t)((hot - (uint32_t)t) & 0x1FFFFFFFu);
+                switch (mode) {
+                case ML2WAIT: ready = r29; break;
+                case MWAITDIR: tag = cold.z; break;
+                case MWAITDATA: tag = cold.z; rx = cold.w >> 1; break;
+                default: ready = r29; tag = cold.z; inst = cold.w & 1u; break;
+                }
+                TupleHash th(6);
+                th.add(mode).add(ready).add(tag).add(inst).add(start).add(rx);
+                H += hterm(D_CORE, n, th.h);
+            }
+            const uint4 *L = S.l2 + (size_t)l * S.sets * S.ways;
+            for (uint32_t i = 0; i < S.sets * S.ways; ++i) {
+                uint4 v = L[i];
+                if (v.x == 0u) continue;
+                uint64_t stamp = ((uint64_t)v.z << 32) | v.y;
+                H += hterm(D_L2, (n * S.sets) * S.ways + i, TupleHash(2).add(v.x - 1u).add(stamp).h);
+            }
+        }
+        if (S.has_script) {
+            uint32_t pos = S.script_pos[l];
+            if (pos) H += hterm(D_SCRIPT, n, TupleHash(1).add(pos).h);
+        }
+    }
+    // block reduction of a u64 sum (mod 2^64)
+    __shared__ unsigned long long red[32];
+    unsigned long long v = H;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (threadIdx.x == 0) atomicAdd(out, v);
+    }
+}
+
+// LOC terms: entries loc[q][lh] != 0, tag T = q*N + n0 + lh.
+__global__ void k_hash_loc(Dev S, unsigned long long *out)
+{
+    uint64_t H = 0;
+    const uint64_t total = (uint64_t)S.tpn * S.nloc;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t e = S.loc[i];
+        if (!e) continue;
+        uint64_t q = i / S.nloc, lh = i - q * S.nloc;
+        uint64_t T = q * S.N + S.n0 + lh;
+        H += hterm(D_LOC, T, TupleHash(2).add(e & HOLDER_MASK).add(e >> HOLDER_BITS).h);
+    }
+    __shared__ unsigned long long red[32];
+    unsigned long long v = H;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (threadIdx.x == 0) atomicAdd(out, v);
+    }
+}
+
+// ------------------------------------------------------------------ launch wrappers
+cudaError_t launch_step(const Dev &S, uint64_t t, uint32_t *activity, cudaStream_t st)
+{
+    uint32_t grid = (S.nloc + 255u) / 256u;
+    if (S.mode == 1u) k_step<1><<<grid, 256, 0, st>>>(S, t, activity);
+    else k_step<0><<<grid, 256, 0, st>>>(S, t, activity);
+    return cudaGetLastError();
+}
+
+size_t persist_smem_bytes(const Dev &S, bool with_hist)
+{
+    return sizeof(unsigned int) * (NCOUNTERS + (with_hist ? 3u * S.nb : 0u));
+}
+
+cudaError_t persist_configure(const Dev &S, int device, uint32_t *grid, uint32_t *nodes_per_cta, uint32_t *smem_hist)
+{
+    int sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    bool with_hist = 3u * S.nb * 4u <= 64u * 1024u;
+    size_t smem = persist_smem_bytes(S, with_hist);
+    const void *fn = S.mode == 1u ? (const void *)k_persist<1> : (const void *)k_persist<0>;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PERSIST_BLOCK, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    uint64_t max_ctas = (uint64_t)sms * (uint64_t)per_sm;
+    uint32_t npc = PERSIST_BLOCK;                     // one node per thread when possible
+    uint64_t g = (S.nloc + npc - 1u) / npc;
+    if (g > max_ctas) {
+        npc = (uint32_t)((S.nloc + max_ctas - 1u) / max_ctas);
+        g = (S.nloc + npc - 1u) / npc;
+    }
+    *grid = (uint32_t)g;
+    *nodes_per_cta = npc;
+    *smem_hist = with_hist ? 1u : 0u;
+    return cudaSuccess;
+}
+
+cudaError_t launch_persist(const Dev &S, uint64_t t0, uint32_t ncyc, uint32_t *progress, uint32_t pbase,
+                           uint32_t grid, uint32_t nodes_per_cta, uint32_t smem_hist, uint32_t *activity,
+                           cudaStream_t st)
+{
+    size_t smem = persist_smem_bytes(S, smem_hist != 0);
+    Dev Sc = S;
+    void *args[] = {(void *)&Sc, (void *)&t0, (void *)&ncyc, (void *)&progress, (void *)&pbase,
+                    (void *)&nodes_per_cta, (void *)&smem_hist, (void *)&activity};
+    const void *fn = S.mode == 1u ? (const void *)k_persist<1> : (const void *)k_persist<0>;
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(PERSIST_BLOCK), args, smem, st);
+}
+
+cudaError_t launch_busy_count(const Dev &S, uint64_t t, uint32_t *out, cudaStream_t st)
+{
+    uint32_t grid = (S.nloc + 255u) / 256u;
+    k_busy_count<<<grid, 256, 0, st>>>(S, t, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hash(const Dev &S, uint64_t t, unsigned long long *out, cudaStream_t st)
+{
+    uint32_t grid = (S.nloc + 255u) / 256u;
+    k_hash_nodes<<<grid, 256, 0, st>>>(S, t, out);
+    if (S.mode == 1u) k_hash_loc<<<1024, 256, 0, st>>>(S, out);
+    return cudaGetLastError();
+}
+
+}  // namespace noc

@@ -1,0 +1,485 @@
+// node_logic.cuh -- the per-cycle, per-node step as
+// device functions, shared by every engine (per-cycle launches, persistent
+// kernels).  One CUDA thread advances one node through Phase 1 (core step,
+// P:L257), Phase 2 (rank + port assignment / deflection) and
+// Phase 3 (eject, reassembly, directory / L2 service, Fig. 4)
+// of cycle t.  All cross-node communication goes through the double-buffered
+// link slots of cycle t+1; everything else a node touches is owned by it
+// (SURVEY 8(c.5)), so no atomics touch the datapath: atomics are used only for
+// the order-independent statistics.
+#pragma once
+#include "common.cuh"
+
+namespace noc {
+
+// Statistic sink.  Rare counters / histogram bins go to shared memory (u32)
+// when the kernel provides it, else straight to global u64 atomics.
+struct Sink {
+    unsigned int *scnt;    // [NCOUNTERS] or nullptr
+    unsigned int *shist;   // [3][nb] or nullptr
+    __device__ __forceinline__ void cnt(const Dev &S, uint32_t i, uint32_t v = 1u) const
+    {
+        if (scnt) atomicAdd(&scnt[i], v);
+        else atomicAdd(&S.cnt[i], (unsigned long long)v);
+    }
+    __device__ __forceinline__ void hist(const Dev &S, uint32_t h, uint32_t v) const
+    {
+        uint32_t b = v < S.nb - 1u ? v : S.nb - 1u;
+        if (shist) atomicAdd(&shist[h * S.nb + b], 1u);
+        else atomicAdd(&S.hist[(size_t)h * S.nb + b], 1ull);
+    }
+};
+
+// Hot counters accumulated in registers and reduced once per launch.
+struct Acc {
+    uint32_t injected, ejected, hops, defl;
+};
+
+// Registers of one node for one cycle.
+struct NodeCtx {
+    uint32_t l, n, x, y;
+    uint32_t qctl;
+    uint32_t hot;
+    uint4 cold;
+    bool q_dirty, hot_dirty, cold_dirty, cold_loaded;
+    bool busy_flit;      // sent a flit this cycle (drain detection)
+};
+
+__device__ __forceinline__ void load_cold(const Dev &S, NodeCtx &c)
+{
+    if (!c.cold_loaded) { c.cold = S.core_cold[c.l]; c.cold_loaded = true; }
+}
+
+__device__ __forceinline__ void set_mode(NodeCtx &c, uint32_t mode, uint64_t ready)
+{
+    c.hot = (mode << 29) | ((uint32_t)ready & 0x1FFFFFFFu);
+    c.hot_dirty = true;
+}
+
+// ENQ (DESIGN 3.3; bounded send FIFO, R21)
+__device__ __forceinline__ void enq(const Dev &S, const Sink &K, NodeCtx &c, uint32_t kind, uint32_t dst,
+                                    uint32_t payload, uint32_t nfl)
+{
+    uint32_t h = q_head(c.qctl), cnt = q_count(c.qctl);
+    if (cnt == S.qcap) { K.cnt(S, C_DROPS + kind); return; }
+    uint32_t slot = (h + cnt) & (S.qcap - 1u);
+    S.fifo_pkt[(size_t)c.l * S.qcap + slot] = make_uint2(dst | (kind << 21) | (nfl << 24), payload);
+    c.qctl = q_make(h, cnt + 1u, q_next(c.qctl));
+    c.q_dirty = true;
+    K.cnt(S, C_ENQ);
+}
+
+__device__ __forceinline__ size_t loc_index(const Dev &S, uint32_t T)
+{
+    uint32_t q = T / S.N, h = T - q * S.N;
+    return (size_t)q * S.nloc + (h - S.n0);
+}
+
+// L2HIT: stamp update on a hit (R23)
+__device__ __forceinline__ bool l2_hit(const Dev &S, const NodeCtx &c, uint32_t T, uint64_t t)
+{
+    uint32_t set = T % S.sets;
+    uint4 *L = S.l2 + ((size_t)c.l * S.sets + set) * S.ways;
+    for (uint32_t w = 0; w < S.ways; ++w) {
+        uint4 v = L[w];
+        if (v.x == T + 1u) {
+            L[w] = make_uint4(v.x, (uint32_t)t, (uint32_t)(t >> 32), 0u);
+            return true;
+        }
+    }
+    return false;
+}
+
+// EVHANDLER at home (R13)
+__device__ __forceinline__ void ev_handler(const Dev &S, const Sink &K, uint32_t T, uint32_t src)
+{
+    size_t i = loc_index(S, T);
+    uint32_t e = S.loc[i];
+    uint32_t h1 = e & HOLDER_MASK, pend = e >> HOLDER_BITS;
+    if (h1 != src + 1u) atomicOr(S.err, ERR_EVHOLDER);
+    if (pend > 0) --pend;
+    else h1 = 0;
+    S.loc[i] = h1 | (pend << HOLDER_BITS);
+    K.cnt(S, C_EVRCVD);
+}
+
+// INSTALL (victim: first invalid, else min stamp, ties lowest way, R23)
+__device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+{
+    uint32_t set = T % S.sets;
+    uint4 *L = S.l2 + ((size_t)c.l * S.sets + set) * S.ways;
+    uint32_t victim = 0;
+    uint64_t best = ~0ull;
+    bool found_invalid = false;
+    uint4 vline = make_uint4(0, 0, 0, 0);
+    for (uint32_t w = 0; w < S.ways; ++w) {
+        uint4 v = L[w];
+        if (v.x == 0u) {
+            if (!found_invalid) { victim = w; vline = v; found_invalid = true; }
+        } else if (!found_invalid) {
+            uint64_t st = ((uint64_t)v.z << 32) | v.y;
+            if (st < best) { best = st; victim = w; vline = v; }
+        }
+    }
+    if (vline.x != 0u) {
+        uint32_t V = vline.x - 1u;
+        uint32_t hv = V % S.N;
+        K.cnt(S, C_EVICTIONS);
+        K.cnt(S, C_EVSENT);
+        if (hv == c.n) ev_handler(S, K, V, c.n);
+        else enq(S, K, c, KEV, hv, V, 1u);
+    }
+    L[victim] = make_uint4(T + 1u, (uint32_t)t, (uint32_t)(t >> 32), 0u);
+    K.cnt(S, C_INSTALLS);
+}
+
+__device__ __forceinline__ void complete(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
+{
+    load_cold(S, c);
+    uint64_t start = ((uint64_t)c.cold.y << 32) | c.cold.x;
+    uint64_t lat = t - start;
+    K.hist(S, 2, lat > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)lat);
+    K.cnt(S, C_COMPLETED);
+    set_mode(c, MIDLE, 0);
+}
+
+__device__ __forceinline__ void receive_ndr(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
+{
+    if (core_mode(c.hot) != MWAITDIR) atomicOr(S.err, ERR_PROTO);
+    K.cnt(S, C_MEMREQ);
+    load_cold(S, c);
+    c.cold.w = (c.cold.w & ~1u) | 1u;          // install = 1
+    c.cold_dirty = true;
+    set_mode(c, MMEMWAIT, t + S.mem_lat);
+}
+
+__device__ __forceinline__ void receive_dr(const Dev &S, const Sink &K, NodeCtx &c, uint32_t holder)
+{
+    if (core_mode(c.hot) != MWAITDIR) atomicOr(S.err, ERR_PROTO);
+    K.cnt(S, C_REQMADE);
+    load_cold(S, c);
+    enq(S, K, c, KRQ, holder, c.cold.z, 1u);
+    set_mode(c, MWAITDATA, 0);
+}
+
+// DIRSERVICE at home c.n for requester r (Fig. 4 steps 1-2; R12-R14, R28)
+__device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t r, uint64_t t)
+{
+    K.cnt(S, C_DIRSEARCH);
+    size_t i = loc_index(S, T);
+    uint32_t e = S.loc[i];
+    uint32_t h1 = e & HOLDER_MASK, pend = e >> HOLDER_BITS;
+    uint32_t kind, payload;
+    if (h1 == 0u) {
+        h1 = r + 1u; kind = KNDR; payload = T;
+    } else if (h1 == r + 1u) {
+        ++pend;
+        if (pend > PEND_MAX) { atomicOr(S.err, ERR_PEND); pend = PEND_MAX; }
+        kind = KNDR; payload = T;
+    } else {
+        kind = KDR; payload = h1 - 1u;
+    }
+    S.loc[i] = h1 | (pend << HOLDER_BITS);
+    if (r == c.n) {
+        if (kind == KNDR) receive_ndr(S, K, c, t);
+        else receive_dr(S, K, c, payload);
+    } else {
+        enq(S, K, c, kind, r, payload, 1u);
+    }
+}
+
+__device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+{
+    load_cold(S, c);
+    c.cold = make_uint4((uint32_t)t, (uint32_t)(t >> 32), T, 0u);   // start, tag, install 0, rx 0
+    c.cold_dirty = true;
+    K.cnt(S, C_ACCESSES);
+    if (l2_hit(S, c, T, t)) {
+        K.cnt(S, C_L2HIT);
+        if (S.l2_hit_lat == 0u) {
+            set_mode(c, MIDLE, 0);
+            K.hist(S, 2, 0u);
+            K.cnt(S, C_COMPLETED);
+        } else {
+            set_mode(c, ML2WAIT, t + S.l2_hit_lat);
+        }
+    } else {
+        K.cnt(S, C_L2MISS);
+        set_mode(c, MWAITDIR, 0);
+        uint32_t h = T % S.N;
+        if (h == c.n) dir_service(S, K, c, T, c.n, t);
+        else enq(S, K, c, KDA, h, T, 1u);
+    }
+}
+
+// Next due script event (DESIGN 3.3).  Returns true and the value if one is consumed.
+__device__ __forceinline__ bool script_next(const Dev &S, const NodeCtx &c, uint64_t t, uint32_t &value)
+{
+    uint32_t off = S.script_off[c.l], end = S.script_off[c.l + 1];
+    uint32_t pos = S.script_pos[c.l];
+    if (off + pos >= end) return false;
+    uint4 ev = S.script[off + pos];
+    uint64_t cyc = ((uint64_t)ev.y << 32) | ev.x;
+    if (cyc > t) return false;
+    value = ev.z;
+    S.script_pos[c.l] = pos + 1u;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Phase 1
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void phase1_ur(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
+{
+    if (!S.gen) return;
+    uint32_t v, dst = 0;
+    bool fire = false;
+    if (S.has_script && script_next(S, c, t, v)) {
+        fire = true; dst = v;
+    } else {
+        uint32_t r[4];
+        philox4x32_10(S.seed_lo, S.seed_hi, c.n, (uint32_t)t, (uint32_t)(t >> 32), 0u, r);
+        if (r[0] < S.thr_inj) {
+            uint32_t d = mulhi32(r[1], S.N - 1u);
+            d += (d >= c.n);
+            fire = true; dst = d;
+        }
+    }
+    if (fire) {
+        K.cnt(S, C_GENERATED);
+        enq(S, K, c, KPROBE, dst, 0u, 1u);
+    }
+}
+
+__device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
+{
+    uint32_t mode = core_mode(c.hot);
+    if ((mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {
+        if (mode == MMEMWAIT) {
+            load_cold(S, c);
+            if (c.cold.w & 1u) install(S, K, c, c.cold.z, t);
+        }
+        complete(S, K, c, t);
+        mode = MIDLE;
+    }
+    if (mode == MIDLE && S.gen) {
+        uint32_t v, T = 0;
+        bool fire = false;
+        if (S.has_script && script_next(S, c, t, v)) {
+            fire = true; T = v;
+        } else {
+            uint32_t r[4];
+            philox4x32_10(S.seed_lo, S.seed_hi, c.n, (uint32_t)t, (uint32_t)(t >> 32), 0u, r);
+            if (r[0] < S.thr_inj) {
+                fire = true;
+                if (r[1] < S.thr_priv) T = c.n * S.tpn + mulhi32(r[2], S.priv);
+                else T = mulhi32(r[2], S.N) * S.tpn + S.priv + mulhi32(r[3], S.tpn - S.priv);
+            }
+        }
+        if (fire) start_access(S, K, c, T, t);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 2: rank and port selection (PMDR P:L116)
+// ---------------------------------------------------------------------------
+// true if a ranks before b at cycle t (R1, R2)
+__device__ __forceinline__ bool ranks_before(uint32_t prio, const Flit &a, const Flit &b, uint32_t t32)
+{
+    if (prio == 0u) {
+        uint32_t aa = f_age(a), ab = f_age(b);
+        if (aa != ab) return aa > ab;
+    }
+    uint32_t la = t32 - a.z, lb = t32 - b.z;     // lifetimes: older = larger
+    if (la != lb) return la > lb;
+    return f_src(a) < f_src(b);
+}
+
+// Output callback: Out(port, flit) stores a routed flit into the next-cycle slot.
+template <typename Out>
+__device__ __forceinline__ void route(const Dev &S, NodeCtx &c, Flit *F, uint32_t nf, uint64_t t, Acc &acc,
+                                      Flit &ej, bool &has_ej, Out &&out)
+{
+    uint32_t t32 = (uint32_t)t;
+    uint32_t ord[5] = {0, 1, 2, 3, 4};
+    // insertion sort of <= 5 indices
+    for (uint32_t i = 1; i < nf; ++i) {
+        uint32_t k = ord[i];
+        uint32_t j = i;
+        while (j > 0 && ranks_before(S.prio, F[k], F[ord[j - 1]], t32)) { ord[j] = ord[j - 1]; --j; }
+        ord[j] = k;
+    }
+    uint32_t exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) |
+                     (c.x > 0 ? 8u : 0u);
+    uint32_t used = 0;
+    has_ej = false;
+    for (uint32_t i = 0; i < nf; ++i) {
+        Flit f = F[ord[i]];
+        uint32_t dst = f_dst(f);
+        if (dst == c.n && !has_ej) { ej = f; has_ej = true; continue; }
+        int p = -1;
+        if (dst != c.n) {
+            uint32_t dy = dst / S.W, dx = dst - dy * S.W;
+            if (dx != c.x) {
+                uint32_t xp = dx > c.x ? PE : PW;
+                if (!(used & (1u << xp))) p = (int)xp;
+            }
+            if (p < 0 && dy != c.y) {
+                uint32_t yp = dy > c.y ? PS : PN;
+                if (!(used & (1u << yp))) p = (int)yp;
+            }
+        }
+        if (p < 0) {
+            uint32_t freep = exist & ~used;            // first free existing port in N,S,E,W (R5)
+            p = (int)(__ffs(freep) - 1);
+            uint32_t a = f_age(f) + 1u;
+            if (a > AGE_MAX) { atomicOr(S.err, ERR_AGE); a = AGE_MAX; }
+            f_set_age(f, a);
+            ++acc.defl;
+        }
+        used |= 1u << p;
+        ++acc.hops;
+        out((uint32_t)p, f);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 3: eject + service
+// ---------------------------------------------------------------------------
+__device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Flit &f, uint64_t t, Acc &acc)
+{
+    ++acc.ejected;
+    K.hist(S, 0, (uint32_t)t - f.z);
+    K.hist(S, 1, f_age(f));
+    switch (f_kind(f)) {
+    case KPROBE:
+        K.cnt(S, C_PROBES);
+        break;
+    case KDA:
+        dir_service(S, K, c, f.w, f_src(f), t);
+        break;
+    case KDR:
+        receive_dr(S, K, c, f.w);
+        break;
+    case KNDR:
+        receive_ndr(S, K, c, t);
+        break;
+    case KRQ:
+        K.cnt(S, C_REQRCVD);
+        if (l2_hit(S, c, f.w, t)) {
+            K.cnt(S, C_REPSENT);
+            enq(S, K, c, KRA, f_src(f), f.w, S.nfl_ra);
+        } else {
+            K.cnt(S, C_TRAPSENT);
+            enq(S, K, c, KTRAP, f_src(f), f.w, 1u);
+        }
+        break;
+    case KRA: {
+        if (core_mode(c.hot) != MWAITDATA) atomicOr(S.err, ERR_PROTO);
+        load_cold(S, c);
+        uint32_t rx = (c.cold.w >> 1) + 1u;
+        if (rx == S.nfl_ra) {
+            c.cold.w &= 1u;
+            c.cold_dirty = true;
+            K.cnt(S, C_REPRCVD);
+            complete(S, K, c, t);
+        } else {
+            c.cold.w = (c.cold.w & 1u) | (rx << 1);
+            c.cold_dirty = true;
+        }
+        break;
+    }
+    case KTRAP:
+        if (core_mode(c.hot) != MWAITDATA) atomicOr(S.err, ERR_PROTO);
+        K.cnt(S, C_TRAPRCVD);
+        K.cnt(S, C_MEMREQ);
+        load_cold(S, c);
+        c.cold.w &= ~1u;                          // install = 0 (R16)
+        c.cold_dirty = true;
+        set_mode(c, MMEMWAIT, t + S.mem_lat);
+        break;
+    default:  // KEV
+        ev_handler(S, K, f.w, f_src(f));
+        break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The whole node step of cycle t with links in global memory (SoA).
+// Returns true if the node is busy at the end of the cycle (drain detection).
+// ---------------------------------------------------------------------------
+template <uint32_t MODE>
+__device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, uint32_t l, uint64_t t, Acc &acc)
+{
+    NodeCtx c;
+    c.l = l;
+    c.n = S.n0 + l;
+    c.y = c.n / S.W;
+    c.x = c.n - c.y * S.W;
+    c.qctl = S.fifo_ctl[l];
+    c.hot = MODE == 1u ? S.core_hot[l] : 0u;
+    c.q_dirty = c.hot_dirty = c.cold_dirty = c.cold_loaded = false;
+    c.busy_flit = false;
+
+    // Phase 1
+    if (MODE == 0u) phase1_ur(S, K, c, t);
+    else phase1_lspd(S, K, c, t);
+
+    // Phase 2: latch inputs of cycle t
+    const uint32_t b = (uint32_t)t & 1u, nb1 = b ^ 1u;
+    const uint32_t st = stamp_of(t);
+    uint32_t fl = __ldcg(&S.flag[b][l]);
+    Flit F[5];
+    uint32_t nf = 0;
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d) {
+        if (((fl >> (8u * d)) & 0xFFu) == st) {
+            uint4 v = __ldcg(&S.flit[b][(size_t)d * S.nloc + l]);
+            F[nf].x = v.x; F[nf].y = v.y; F[nf].z = v.z; F[nf].w = v.w;
+            ++nf;
+        }
+    }
+    uint32_t deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
+    uint32_t qn = q_count(c.qctl);
+    if (nf < deg && qn > 0) {
+        uint32_t h = q_head(c.qctl), nx = q_next(c.qctl);
+        uint2 p = S.fifo_pkt[(size_t)l * S.qcap + h];
+        uint32_t nfl = (p.x >> 24) & 15u;
+        F[nf++] = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
+        ++acc.injected;
+        ++nx;
+        if (nx == nfl) c.qctl = q_make((h + 1u) & (S.qcap - 1u), qn - 1u, 0u);
+        else c.qctl = q_make(h, qn, nx);
+        c.q_dirty = true;
+    }
+    Flit ej;
+    bool has_ej = false;
+    if (nf) {
+        const uint8_t st1 = stamp_of(t + 1);
+        route(S, c, F, nf, t, acc, ej, has_ej, [&](uint32_t p, const Flit &f) {
+            // neighbour's local index and its input slot opp(p)
+            uint32_t m, slot;
+            switch (p) {
+            case PN: m = l - S.W; slot = PS; break;
+            case PS: m = l + S.W; slot = PN; break;
+            case PE: m = l + 1u; slot = PW; break;
+            default: m = l - 1u; slot = PE; break;
+            }
+            S.flit[nb1][(size_t)slot * S.nloc + m] = make_uint4(f.x, f.y, f.z, f.w);
+            reinterpret_cast<uint8_t *>(S.flag[nb1])[(size_t)m * 4u + slot] = st1;
+        });
+        c.busy_flit = nf > (has_ej ? 1u : 0u);
+    }
+
+    // Phase 3
+    if (has_ej) phase3(S, K, c, ej, t, acc);
+
+    if (c.q_dirty) S.fifo_ctl[l] = c.qctl;
+    if (MODE == 1u) {
+        if (c.hot_dirty) S.core_hot[l] = c.hot;
+        if (c.cold_dirty) S.core_cold[l] = c.cold;
+    }
+    return c.busy_flit || q_count(c.qctl) > 0 || core_mode(c.hot) != MIDLE;
+}
+
+}  // namespace noc

@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bit-exact on every counter, the three histograms and the canonical state
+hash (the model is integer and deterministic, DESIGN 3).
+All tests need a B200 (sm_100a).
+"""
+import collections
+import random
+
+import pytest
+
+import paper_1508_03235_b200 as nb
+from paper_1508_03235_b200 import workloads as W
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = [nb.ENGINE_STEP, nb.ENGINE_PERSIST]
+
+
+def both(cfg, cycles, engine=nb.ENGINE_AUTO, script=None, drain=None, split=None):
+    g = nb.NocSim(cfg, script=script, engine=engine)
+    o = Oracle(cfg, script=script)
+    for k in (split or [cycles]):
+        g.run(k)
+        o.run(k)
+    if drain is not None:
+        assert g.drain(drain) == o.drain(drain)
+    return g, o
+
+
+def assert_same(g, o):
+    gs, os_ = g.stats(), o.stats()
+    assert gs[0] == os_[0], {k: (gs[0][k], os_[0][k]) for k in gs[0] if gs[0][k] != os_[0][k]}
+    for i, name in ((1, "lat"), (2, "defl"), (3, "acc")):
+        if gs[i] != os_[i]:
+            diff = {b: (x, y) for b, (x, y) in enumerate(zip(gs[i], os_[i])) if x != y}
+            raise AssertionError("hist %s differs at %s" % (name, dict(list(diff.items())[:10])))
+    assert g.state_hash() == o.state_hash()
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_c1a_uniform_random_4x4(engine, seed):
+    """BASELINE configs[0]: 4x4, 0.1 flits/node/cycle, 10k cycles."""
+    g, o = both(W.c1a(seed=seed), 10_000, engine)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_c1b_lspd_4x4(engine, seed):
+    g, o = both(W.c1b(seed=seed), 10_000, engine)
+    assert_same(g, o)
+    st = g.stats()[0]
+    assert st["replies_sent"] > 0 and st["traps_sent"] > 0 and st["evictions"] > 0
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("prio", [W.PRIO_DEFLECT, W.PRIO_OLDEST])
+def test_saturated_ur_with_drops(engine, prio):
+    """Saturated 16x16 UR (deflection regime, FIFO overflow drops)."""
+    cfg = W.make(mesh_w=16, mesh_h=16, mode=W.MODE_UR, lam=0.5, prio=prio, sendq_cap=4)
+    g, o = both(cfg, 3000, engine)
+    assert_same(g, o)
+    assert g.stats()[0]["drops_probe"] > 0
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c2_64x64_lspd(engine):
+    """BASELINE configs[1] geometry (64x64 LSPD), shortened run (oracle time)."""
+    g, o = both(W.c2(), 6000, engine)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c3_208x208_lspd_bench_config(engine):
+    """The bench workload (208x208 LSPD, seed 1) in the launch configuration
+    bench.py times, oracle-checked over a window the oracle finishes in
+    seconds."""
+    g, o = both(W.c3(), 1500, engine)
+    assert_same(g, o)
+
+
+def test_c4_saturated_208():
+    cfg = W.c4(0.3)
+    g, o = both(cfg, 400, nb.ENGINE_PERSIST)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("cfg", [
+    W.make(mesh_w=2, mesh_h=2, mode=W.MODE_UR, lam=0.7),
+    W.make(mesh_w=2, mesh_h=37, mode=W.MODE_UR, lam=0.3, prio=W.PRIO_OLDEST),
+    W.make(mesh_w=53, mesh_h=3, mode=W.MODE_LSPD, lam=0.2, l2_sets=3, l2_ways=3, sendq_cap=32),
+    W.make(mesh_w=5, mesh_h=7, mode=W.MODE_LSPD, lam=0.5, l2_hit_lat=0, nfl_ra=1, sendq_cap=32),
+    W.make(mesh_w=6, mesh_h=6, mode=W.MODE_LSPD, lam=0.3, nfl_ra=8, sendq_cap=2, hist_bins=1),
+    W.make(mesh_w=9, mesh_h=4, mode=W.MODE_LSPD, lam=1.0, l2_sets=1, l2_ways=16, sendq_cap=64,
+           tags_per_node=4, priv_tags=1, mem_lat=1),
+    W.make(mesh_w=300, mesh_h=7, mode=W.MODE_LSPD, lam=0.1, hist_bins=64, seed=2 ** 40 + 7),
+], ids=["2x2", "2x37-oldest", "53x3", "hitlat0-nfl1", "nfl8-q2-nb1", "1set16way", "300x7-bigseed"])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_edge_configurations(cfg, engine):
+    g, o = both(cfg, 2500, engine)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_split_runs_and_drain(engine):
+    """run(a); run(b) == run(a+b) and drain (R30) on both sides."""
+    cfg = W.make(mesh_w=12, mesh_h=10, mode=W.MODE_LSPD, lam=0.2, sendq_cap=32, l2_sets=4)
+    g, o = both(cfg, None, engine, split=[1, 700, 1299], drain=100000)
+    assert_same(g, o)
+    st = g.stats()[0]
+    assert st["requests_made"] == st["requests_received"] and st["accesses"] == st["completed"]
+    g.run(500)
+    o.run(500)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_drain_cap_and_already_quiescent(engine):
+    cfg = W.make(mesh_w=8, mesh_h=8, mode=W.MODE_UR, lam=0.5)
+    g, o = both(cfg, 1000, engine)
+    assert g.drain(3) == o.drain(3) == (3, False)
+    assert_same(g, o)
+    r = g.drain(10 ** 6)
+    assert r == o.drain(10 ** 6) and r[1]
+    assert g.drain(10) == o.drain(10) == (0, True)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_scripted_events(engine):
+    for cfg in (W.make(mesh_w=10, mesh_h=9, mode=W.MODE_UR, lam=0.05),
+                W.make(mesh_w=10, mesh_h=9, mode=W.MODE_LSPD, lam=0.05, sendq_cap=32)):
+        script = W.random_script(cfg, 3000, 2000, seed=5)
+        g, o = both(cfg, 2500, engine, script=script)
+        assert_same(g, o)
+
+
+def test_engines_agree_on_hash():
+    cfg = W.lspd(40, 33, lam=0.1, seed=9)
+    hs = []
+    for e in ENGINES:
+        g = nb.NocSim(cfg, engine=e)
+        g.run(3000)
+        hs.append(g.state_hash())
+    assert len(set(hs)) == 1
+
+
+def test_zero_load_latency_208():
+    """Closed form at the full bench mesh: lone flits take Manhattan hops."""
+    rng = random.Random(3)
+    w = h = 208
+    n = w * h
+    gap = w + h + 2
+    pairs = []
+    for _ in range(300):
+        s = rng.randrange(n)
+        d = rng.randrange(n - 1)
+        pairs.append((s, d + (d >= s)))
+    script = [(k * gap, s, d) for k, (s, d) in enumerate(pairs)]
+    g = nb.NocSim(W.make(mesh_w=w, mesh_h=h, mode=W.MODE_UR, thr_inj=0), script=script)
+    g.run(len(pairs) * gap)
+    hl = g.stats()[1]
+    want = collections.Counter(abs(s % w - d % w) + abs(s // w - d // w) for s, d in pairs)
+    assert {b: c for b, c in enumerate(hl) if c} == dict(want)
+
+
+def test_c3_long_run_properties():
+    """Full-length properties at the bench size (any length): conservation
+    after drain and the Table II equalities; no FIFO drops."""
+    g = nb.NocSim(W.c3())
+    g.run(20_000)
+    used, drained = g.drain(100_000)
+    st = g.stats()[0]
+    assert drained
+    assert st["injected"] == st["ejected"]
+    assert st["requests_made"] == st["requests_received"]
+    assert st["replies_sent"] == st["replies_received"]
+    assert st["traps_sent"] == st["traps_received"]
+    assert st["evs_sent"] == st["evs_received"]
+    assert st["accesses"] == st["completed"]
+    assert sum(v for k, v in st.items() if k.startswith("drops_")) == 0
