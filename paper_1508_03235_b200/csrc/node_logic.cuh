@@ -429,6 +429,9 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
     const uint32_t b = (uint32_t)t & 1u, nb1 = b ^ 1u;
     const uint32_t st = stamp_of(t);
     uint32_t fl = __ldcg(&S.flag[b][l]);
+    // consume: clear the occupancy word (its slots are re-written for cycle t+2
+    // only after the cycle boundary), so a stale stamp can never match again
+    if (fl) S.flag[b][l] = 0u;
     Flit F[5];
     uint32_t nf = 0;
 #pragma unroll
