@@ -174,7 +174,7 @@ def run_ours(args):
     # engine is built: weak scaling, no data-path collective.
     cfg = fn(seed=1 + rank)
     n = cfg["mesh_w"] * cfg["mesh_h"]
-    eng = {"auto": pkg.ENGINE_AUTO, "step": pkg.ENGINE_STEP, "persist": pkg.ENGINE_PERSIST}[args.engine]
+    eng = {"auto": pkg.ENGINE_AUTO, "step": pkg.ENGINE_STEP, "persist": pkg.ENGINE_PERSIST, "tiled": pkg.ENGINE_TILED}[args.engine]
     sim = pkg.NocSim(cfg, device=dev, engine=eng)
     cyc = args.cycles_per_step
     l2buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if not args.no_flush else None
@@ -247,7 +247,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_persist" if info1["engine"] == 2 else "k_step",
+                     "kernel": {1: "k_step", 2: "k_persist", 3: "k_tiled"}[info1["engine"]],
                      "bytes_per_node_cycle": B, "rates": rates, "per_launch_ms": per_launch_ms},
         "clocks": ck,
         "sim": {"hash": None, "drops": sum(v for k, v in delta.items() if k.startswith("drops_"))},
@@ -275,7 +275,7 @@ def main():
     ap.add_argument("--cycles-per-step", type=int, default=2000)
     ap.add_argument("--ref-cycles-per-step", type=int, default=200)
     ap.add_argument("--cpu-cycles", type=int, default=2000)
-    ap.add_argument("--engine", default="auto", choices=["auto", "step", "persist"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "step", "persist", "tiled"])
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

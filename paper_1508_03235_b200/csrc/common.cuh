@@ -160,11 +160,41 @@ struct Dev {
     unsigned long long *cnt;          // [NCOUNTERS]
     unsigned long long *hist;         // [3][nb]
     uint32_t *err;                    // [1] error flags
-    // halo (multi-GPU row bands; null when the band is the whole mesh)
-    uint4 *halo_out_flit[2];          // [2 sides][W] flits leaving the band (0 = north, 1 = south)
-    uint32_t *halo_out_flag[2];       // [2 sides][W] stamps
+    // TILED engine: TX x TY tiles over the band; links that cross a tile
+    // boundary live in "LL" slots: [2 parity][4 slot][nloc][4 words] u64, each
+    // word = stamp (lo32 = cycle it is an input of) | data (hi32).  Word 0 data
+    // is flit.x or LL_EMPTY; words 1..3 carry flit.y, .z, .w.  Null otherwise.
+    uint32_t TX, TY;
+    unsigned long long *ll;
 };
 
+constexpr uint32_t LL_EMPTY = 0xFFFFFFFFu;   // dst field all ones: never a node (N <= 2^21-1)
+
 __host__ __device__ __forceinline__ uint8_t stamp_of(uint64_t cycle) { return (uint8_t)(0x80u | (cycle & 0x7Fu)); }
+
+// LL word index of (parity b, input slot d, local node l, word w)
+__host__ __device__ __forceinline__ size_t ll_index(const Dev &S, uint32_t b, uint32_t d, uint32_t l, uint32_t w)
+{
+    return (((size_t)b * 4u + d) * S.nloc + l) * 4u + w;
+}
+
+// tile column / row of a mesh coordinate for the TILED engine (x0(tx) = tx*W/TX)
+__host__ __device__ __forceinline__ uint32_t tile_of(uint32_t x, uint32_t W, uint32_t TX)
+{
+    return (uint32_t)((((uint64_t)x + 1u) * TX + W - 1u) / W) - 1u;
+}
+
+// true if input slot d of node (x, y) is fed by a node of another tile
+__host__ __device__ __forceinline__ bool slot_external(const Dev &S, uint32_t x, uint32_t y, uint32_t d)
+{
+    if (!S.ll) return false;
+    const uint32_t ly = y - S.row0;
+    switch (d) {
+    case PN: return y > 0 && tile_of(ly, S.rows, S.TY) != tile_of(ly - 1u, S.rows, S.TY);
+    case PS: return y + 1 < S.H && tile_of(ly, S.rows, S.TY) != tile_of(ly + 1u, S.rows, S.TY);
+    case PE: return x + 1 < S.W && tile_of(x, S.W, S.TX) != tile_of(x + 1u, S.W, S.TX);
+    default: return x > 0 && tile_of(x, S.W, S.TX) != tile_of(x - 1u, S.W, S.TX);
+    }
+}
 
 }  // namespace noc

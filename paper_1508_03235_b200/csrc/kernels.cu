@@ -128,15 +128,38 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, u
             if (shist[i]) atomicAdd(&S.hist[i], (unsigned long long)shist[i]);
 }
 
+// ------------------------------------------------------------------ link state between launches
+// Input slot d of local node l at the boundary before cycle t: a flit, or none.
+// Tile-crossing links of the TILED engine live in LL slots, all others in the
+// flag/flit arrays.
+__device__ bool read_slot(const Dev &S, uint32_t l, uint32_t d, uint64_t t, Flit &f)
+{
+    const uint32_t n = S.n0 + l, y = n / S.W, x = n - y * S.W;
+    const uint32_t b = (uint32_t)t & 1u;
+    if (slot_external(S, x, y, d)) {
+        unsigned long long w0 = S.ll[ll_index(S, b, d, l, 0)];
+        if ((uint32_t)w0 != (uint32_t)t || (uint32_t)(w0 >> 32) == LL_EMPTY) return false;
+        f.x = (uint32_t)(w0 >> 32);
+        f.y = (uint32_t)(S.ll[ll_index(S, b, d, l, 1)] >> 32);
+        f.z = (uint32_t)(S.ll[ll_index(S, b, d, l, 2)] >> 32);
+        f.w = (uint32_t)(S.ll[ll_index(S, b, d, l, 3)] >> 32);
+        return true;
+    }
+    uint32_t fl = S.flag[b][l];
+    if (((fl >> (8u * d)) & 0xFFu) != stamp_of(t)) return false;
+    uint4 v = S.flit[b][(size_t)d * S.nloc + l];
+    f = Flit{v.x, v.y, v.z, v.w};
+    return true;
+}
+
 // ------------------------------------------------------------------ drain helper
 __global__ void k_busy_count(Dev S, uint64_t t, uint32_t *out)
 {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     bool busy = false;
     if (l < S.nloc) {
-        uint32_t fl = S.flag[(uint32_t)t & 1u][l];
-        uint8_t st = stamp_of(t);
-        for (int d = 0; d < 4; ++d) busy |= ((fl >> (8 * d)) & 0xFFu) == st;
+        Flit f;
+        for (uint32_t d = 0; d < 4; ++d) busy |= read_slot(S, l, d, t, f);
         busy |= q_count(S.fifo_ctl[l]) > 0;
         if (S.mode == 1u) busy |= core_mode(S.core_hot[l]) != MIDLE;
     }
@@ -151,13 +174,9 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
     uint64_t H = 0;
     if (l < S.nloc) {
         const uint64_t n = S.n0 + l;
-        const uint32_t b = (uint32_t)t & 1u;
-        const uint8_t st = stamp_of(t);
-        uint32_t fl = S.flag[b][l];
         for (uint32_t d = 0; d < 4; ++d) {
-            if (((fl >> (8u * d)) & 0xFFu) != st) continue;
-            uint4 v = S.flit[b][(size_t)d * S.nloc + l];
-            Flit f{v.x, v.y, v.z, v.w};
+            Flit f;
+            if (!read_slot(S, l, d, t, f)) continue;
             uint64_t life = (uint32_t)((uint32_t)t - f.z);
             uint64_t inj = t - life;
             TupleHash th(7);

@@ -5,6 +5,13 @@
 namespace noc {
 
 constexpr uint32_t PERSIST_BLOCK = 256;
+constexpr uint32_t TILE_MAX_THREADS = 512;
+
+// TILED engine (tile_engine.cu): configure picks the tiling (sets S.TX, S.TY)
+cudaError_t tiled_configure(Dev &S, int device, uint32_t *grid, uint32_t *tpad, uint32_t *smem_hist);
+cudaError_t launch_tiled(const Dev &S, uint64_t t0, uint32_t ncyc, uint32_t grid, uint32_t tpad, uint32_t smem_hist,
+                         uint32_t *activity, cudaStream_t st);
+cudaError_t launch_ll_reset(const Dev &S, uint64_t t, cudaStream_t st);
 
 cudaError_t launch_step(const Dev &S, uint64_t t, uint32_t *activity, cudaStream_t st);
 cudaError_t persist_configure(const Dev &S, int device, uint32_t *grid, uint32_t *nodes_per_cta,

@@ -41,6 +41,8 @@ struct NodeCtx {
     uint32_t qctl;
     uint32_t hot;
     uint4 cold;
+    uint2 head;          // cached head packet of the send FIFO (valid iff head_ok)
+    bool head_ok;
     bool q_dirty, hot_dirty, cold_dirty, cold_loaded;
     bool busy_flit;      // sent a flit this cycle (drain detection)
 };
@@ -63,7 +65,9 @@ __device__ __forceinline__ void enq(const Dev &S, const Sink &K, NodeCtx &c, uin
     uint32_t h = q_head(c.qctl), cnt = q_count(c.qctl);
     if (cnt == S.qcap) { K.cnt(S, C_DROPS + kind); return; }
     uint32_t slot = (h + cnt) & (S.qcap - 1u);
-    S.fifo_pkt[(size_t)c.l * S.qcap + slot] = make_uint2(dst | (kind << 21) | (nfl << 24), payload);
+    const uint2 pkt = make_uint2(dst | (kind << 21) | (nfl << 24), payload);
+    S.fifo_pkt[(size_t)c.l * S.qcap + slot] = pkt;
+    if (cnt == 0u) { c.head = pkt; c.head_ok = true; }
     c.qctl = q_make(h, cnt + 1u, q_next(c.qctl));
     c.q_dirty = true;
     K.cnt(S, C_ENQ);
@@ -104,7 +108,7 @@ __device__ __forceinline__ void ev_handler(const Dev &S, const Sink &K, uint32_t
 }
 
 // INSTALL (victim: first invalid, else min stamp, ties lowest way, R23)
-__device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
 {
     uint32_t set = T % S.sets;
     uint4 *L = S.l2 + ((size_t)c.l * S.sets + set) * S.ways;
@@ -163,7 +167,7 @@ __device__ __forceinline__ void receive_dr(const Dev &S, const Sink &K, NodeCtx 
 }
 
 // DIRSERVICE at home c.n for requester r (Fig. 4 steps 1-2; R12-R14, R28)
-__device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t r, uint64_t t)
+static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t r, uint64_t t)
 {
     K.cnt(S, C_DIRSEARCH);
     size_t i = loc_index(S, T);
@@ -188,7 +192,7 @@ __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T,
     }
 }
 
-__device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+static __device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
 {
     load_cold(S, c);
     c.cold = make_uint4((uint32_t)t, (uint32_t)(t >> 32), T, 0u);   // start, tag, install 0, rx 0
@@ -295,26 +299,46 @@ __device__ __forceinline__ bool ranks_before(uint32_t prio, const Flit &a, const
     return f_src(a) < f_src(b);
 }
 
+// The <= 5 router inputs (4 link slots + the injection slot) held in registers.
+struct Inputs {
+    Flit f[5];
+    uint32_t present;   // bit k: slot k holds a flit
+};
+
+// compare-exchange of slots I, J (I < J): afterwards slot I ranks before slot J;
+// empty slots sink to the end
+template <int I, int J>
+__device__ __forceinline__ void cex(Inputs &in, uint32_t prio, uint32_t t32)
+{
+    const bool pi = (in.present >> I) & 1u, pj = (in.present >> J) & 1u;
+    const bool sw = pj && (!pi || ranks_before(prio, in.f[J], in.f[I], t32));
+    if (sw) {
+        Flit tmp = in.f[I];
+        in.f[I] = in.f[J];
+        in.f[J] = tmp;
+        in.present = (in.present & ~((1u << I) | (1u << J))) | ((uint32_t)pj << I) | ((uint32_t)pi << J);
+    }
+}
+
+// Rank + port selection for the router of node c (R3-R6).
 // Output callback: Out(port, flit) stores a routed flit into the next-cycle slot.
 template <typename Out>
-__device__ __forceinline__ void route(const Dev &S, NodeCtx &c, Flit *F, uint32_t nf, uint64_t t, Acc &acc,
+__device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs &in, uint64_t t, Acc &acc,
                                       Flit &ej, bool &has_ej, Out &&out)
 {
-    uint32_t t32 = (uint32_t)t;
-    uint32_t ord[5] = {0, 1, 2, 3, 4};
-    // insertion sort of <= 5 indices
-    for (uint32_t i = 1; i < nf; ++i) {
-        uint32_t k = ord[i];
-        uint32_t j = i;
-        while (j > 0 && ranks_before(S.prio, F[k], F[ord[j - 1]], t32)) { ord[j] = ord[j - 1]; --j; }
-        ord[j] = k;
-    }
+    const uint32_t t32 = (uint32_t)t;
+    // "Priority Sort": optimal 9-comparator network for 5 inputs
+    cex<0, 1>(in, S.prio, t32); cex<3, 4>(in, S.prio, t32); cex<2, 4>(in, S.prio, t32);
+    cex<2, 3>(in, S.prio, t32); cex<1, 4>(in, S.prio, t32); cex<0, 3>(in, S.prio, t32);
+    cex<0, 2>(in, S.prio, t32); cex<1, 3>(in, S.prio, t32); cex<1, 2>(in, S.prio, t32);
     uint32_t exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) |
                      (c.x > 0 ? 8u : 0u);
     uint32_t used = 0;
     has_ej = false;
-    for (uint32_t i = 0; i < nf; ++i) {
-        Flit f = F[ord[i]];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (!((in.present >> i) & 1u)) break;
+        Flit f = in.f[i];
         uint32_t dst = f_dst(f);
         if (dst == c.n && !has_ej) { ej = f; has_ej = true; continue; }
         int p = -1;
@@ -341,12 +365,13 @@ __device__ __forceinline__ void route(const Dev &S, NodeCtx &c, Flit *F, uint32_
         ++acc.hops;
         out((uint32_t)p, f);
     }
+    return used;   // output ports taken
 }
 
 // ---------------------------------------------------------------------------
 // Phase 3: eject + service
 // ---------------------------------------------------------------------------
-__device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Flit &f, uint64_t t, Acc &acc)
+static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Flit &f, uint64_t t, Acc &acc)
 {
     ++acc.ejected;
     K.hist(S, 0, (uint32_t)t - f.z);
@@ -405,6 +430,34 @@ __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Flit &f, u
 }
 
 // ---------------------------------------------------------------------------
+// Injection (R7, R8): one flit of the head packet per cycle, only
+// if fewer flits than ports arrived.  The injected flit takes slot 4.  When the
+// head packet is popped, the next head is fetched (used at t+1 at the earliest).
+__device__ __forceinline__ void inject(const Dev &S, NodeCtx &c, Inputs &in, uint64_t t, Acc &acc)
+{
+    const uint32_t deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
+    const uint32_t qn = q_count(c.qctl);
+    if (qn == 0u || (uint32_t)__popc(in.present) >= deg) return;
+    const uint32_t h = q_head(c.qctl);
+    uint32_t nx = q_next(c.qctl);
+    if (!c.head_ok) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h]; c.head_ok = true; }
+    const uint2 p = c.head;
+    const uint32_t nfl = (p.x >> 24) & 15u;
+    in.f[4] = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
+    in.present |= 16u;
+    ++acc.injected;
+    ++nx;
+    if (nx == nfl) {
+        const uint32_t h1 = (h + 1u) & (S.qcap - 1u);
+        c.qctl = q_make(h1, qn - 1u, 0u);
+        c.head_ok = qn > 1u;
+        if (c.head_ok) c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h1];
+    } else {
+        c.qctl = q_make(h, qn, nx);
+    }
+    c.q_dirty = true;
+}
+
 // The whole node step of cycle t with links in global memory (SoA).
 // Returns true if the node is busy at the end of the cycle (drain detection).
 // ---------------------------------------------------------------------------
@@ -418,6 +471,7 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
     c.x = c.n - c.y * S.W;
     c.qctl = S.fifo_ctl[l];
     c.hot = MODE == 1u ? S.core_hot[l] : 0u;
+    c.head_ok = false;
     c.q_dirty = c.hot_dirty = c.cold_dirty = c.cold_loaded = false;
     c.busy_flit = false;
 
@@ -432,34 +486,23 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
     // consume: clear the occupancy word (its slots are re-written for cycle t+2
     // only after the cycle boundary), so a stale stamp can never match again
     if (fl) S.flag[b][l] = 0u;
-    Flit F[5];
-    uint32_t nf = 0;
+    Inputs in;
+    in.present = 0;
 #pragma unroll
     for (uint32_t d = 0; d < 4; ++d) {
         if (((fl >> (8u * d)) & 0xFFu) == st) {
             uint4 v = __ldcg(&S.flit[b][(size_t)d * S.nloc + l]);
-            F[nf].x = v.x; F[nf].y = v.y; F[nf].z = v.z; F[nf].w = v.w;
-            ++nf;
+            in.f[d] = Flit{v.x, v.y, v.z, v.w};
+            in.present |= 1u << d;
         }
     }
-    uint32_t deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
-    uint32_t qn = q_count(c.qctl);
-    if (nf < deg && qn > 0) {
-        uint32_t h = q_head(c.qctl), nx = q_next(c.qctl);
-        uint2 p = S.fifo_pkt[(size_t)l * S.qcap + h];
-        uint32_t nfl = (p.x >> 24) & 15u;
-        F[nf++] = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
-        ++acc.injected;
-        ++nx;
-        if (nx == nfl) c.qctl = q_make((h + 1u) & (S.qcap - 1u), qn - 1u, 0u);
-        else c.qctl = q_make(h, qn, nx);
-        c.q_dirty = true;
-    }
+    inject(S, c, in, t, acc);
     Flit ej;
     bool has_ej = false;
-    if (nf) {
+    if (in.present) {
+        const uint32_t nf = __popc(in.present);
         const uint8_t st1 = stamp_of(t + 1);
-        route(S, c, F, nf, t, acc, ej, has_ej, [&](uint32_t p, const Flit &f) {
+        route(S, c, in, t, acc, ej, has_ej, [&](uint32_t p, const Flit &f) {
             // neighbour's local index and its input slot opp(p)
             uint32_t m, slot;
             switch (p) {

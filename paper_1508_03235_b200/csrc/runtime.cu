@@ -42,6 +42,8 @@ struct noc_sim {
     uint32_t *progress = nullptr;
     uint32_t pbase = 0;
     uint32_t p_grid = 0, p_npc = 0, p_smem_hist = 0;
+    // tiled engine
+    uint32_t t_grid = 0, t_tpad = 0, t_smem_hist = 0;
     // scratch
     uint32_t *d_scratch = nullptr;          // [DRAIN_CHUNK + 2]
     unsigned long long *d_hash = nullptr;
@@ -93,7 +95,7 @@ static int validate(const noc_sim_config *c)
     if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size)
         return fail(NOC_EINVAL, "bad world_size/rank");
     if (c->world_size > 1) return fail(NOC_EINVAL, "world_size > 1 is not built into this library version");
-    if (c->engine > NOC_ENGINE_PERSIST) return fail(NOC_EINVAL, "unknown engine");
+    if (c->engine > NOC_ENGINE_TILED) return fail(NOC_EINVAL, "unknown engine");
     for (int i = 0; i < 8; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->n_script && !c->script) return fail(NOC_EINVAL, "n_script > 0 with a null script");
@@ -226,8 +228,32 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     if ((rc = dalloc(s, &s->d_scratch, DRAIN_CHUNK + 2))) return bail(rc);
     if ((rc = dalloc(s, &s->d_hash, 1))) return bail(rc);
 
-    // engine
-    s->engine = cfg->engine == NOC_ENGINE_AUTO ? NOC_ENGINE_PERSIST : cfg->engine;
+    // engine: TILED when every tile fits one CTA of <= TILE_MAX_THREADS
+    // threads on its own SM, else PERSIST (DESIGN 6)
+    s->engine = cfg->engine;
+    if (s->engine == NOC_ENGINE_AUTO || s->engine == NOC_ENGINE_TILED) {
+        Dev trial = D;
+        uint32_t g = 0, tp = 0, sh = 0;
+        cudaError_t ce = tiled_configure(trial, s->device, &g, &tp, &sh);
+        if (ce == cudaSuccess) {
+            s->engine = NOC_ENGINE_TILED;
+            D.TX = trial.TX;
+            D.TY = trial.TY;
+            s->t_grid = g;
+            s->t_tpad = tp;
+            s->t_smem_hist = sh;
+        } else if (s->engine == NOC_ENGINE_TILED) {
+            cudaGetLastError();
+            return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") + cudaGetErrorString(ce)));
+        } else {
+            cudaGetLastError();
+            s->engine = NOC_ENGINE_PERSIST;
+        }
+    }
+    if (s->engine == NOC_ENGINE_TILED) {
+        if ((rc = dalloc(s, &D.ll, (size_t)32u * n))) return bail(rc);
+        if (launch_ll_reset(D, 0, s->stream) != cudaSuccess) return bail(fail(NOC_ECUDA, "ll reset failed"));
+    }
     if (s->engine == NOC_ENGINE_PERSIST) {
         cudaError_t ce = persist_configure(D, s->device, &s->p_grid, &s->p_npc, &s->p_smem_hist);
         if (ce != cudaSuccess) return bail(fail(NOC_ECUDA, std::string("persist_configure: ") + cudaGetErrorString(ce)));
@@ -257,7 +283,17 @@ static int check_err(noc_sim *s)
 static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
 {
     cudaError_t e;
-    if (s->engine == NOC_ENGINE_PERSIST) {
+    if (s->engine == NOC_ENGINE_TILED) {
+        uint64_t done = 0;
+        while (done < n) {
+            uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
+            e = launch_tiled(s->D, s->t + done, k, s->t_grid, s->t_tpad, s->t_smem_hist,
+                             activity ? activity + done : nullptr, s->stream);
+            if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(e));
+            done += k;
+            s->launches += 1;
+        }
+    } else if (s->engine == NOC_ENGINE_PERSIST) {
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
@@ -337,6 +373,9 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
             q = 1;
             k += i + 1;
             s->t = t0 + k;
+            // boundary slots were stamped up to the end of the chunk: re-stamp
+            // them EMPTY for the rewound cycle (nothing is in flight)
+            if (s->engine == NOC_ENGINE_TILED) CU(launch_ll_reset(s->D, s->t, s->stream));
         } else {
             k += chunk;
         }
@@ -400,7 +439,12 @@ extern "C" int noc_sim_get_info(noc_sim *s, noc_sim_info *o)
     if (!s || !o) return fail(NOC_EINVAL, "null argument");
     memset(o, 0, sizeof *o);
     o->engine = s->engine;
-    if (s->engine == NOC_ENGINE_PERSIST) {
+    if (s->engine == NOC_ENGINE_TILED) {
+        o->grid = s->t_grid;
+        o->block = s->t_tpad;
+        o->reserved[0] = (int32_t)s->D.TX;
+        o->reserved[1] = (int32_t)s->D.TY;
+    } else if (s->engine == NOC_ENGINE_PERSIST) {
         o->grid = s->p_grid;
         o->block = PERSIST_BLOCK;
     } else {

@@ -15,7 +15,7 @@ from oracle import Oracle
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = [nb.ENGINE_STEP, nb.ENGINE_PERSIST]
+ENGINES = [nb.ENGINE_STEP, nb.ENGINE_PERSIST, nb.ENGINE_TILED]
 
 
 def both(cfg, cycles, engine=nb.ENGINE_AUTO, script=None, drain=None, split=None):
@@ -182,3 +182,20 @@ def test_c3_long_run_properties():
     assert st["evs_sent"] == st["evs_received"]
     assert st["accesses"] == st["completed"]
     assert sum(v for k, v in st.items() if k.startswith("drops_")) == 0
+
+
+def test_auto_engine_is_tiled_at_bench_size():
+    g = nb.NocSim(W.c3())
+    info = g.info()
+    assert info["engine"] == nb.ENGINE_TILED and info["grid"] <= info["sm_count"]
+
+
+@pytest.mark.parametrize("w,h", [(13, 11), (148, 2), (2, 300), (31, 29)])
+def test_tiled_odd_tilings(w, h):
+    """Tilings with 1-wide tiles, single-row bands and ragged tile sizes."""
+    cfg = W.make(mesh_w=w, mesh_h=h, mode=W.MODE_LSPD, lam=0.3, sendq_cap=32, l2_sets=4, mem_lat=20)
+    g, o = both(cfg, 1500, nb.ENGINE_TILED)
+    assert_same(g, o)
+    cfg = W.make(mesh_w=w, mesh_h=h, mode=W.MODE_UR, lam=0.2)
+    g, o = both(cfg, 1500, nb.ENGINE_TILED)
+    assert_same(g, o)
