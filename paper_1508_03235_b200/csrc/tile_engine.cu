@@ -241,7 +241,12 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
                 }
                 st_relaxed_u64(&S.ll[ll_index(S, nb1, p ^ 1u, m, 0)], llw(st32n, LL_EMPTY));
             }
-            if (has_ej) { pend = ej; has_pend = true; }
+            if (has_ej) {
+                // while draining, quiescence is judged at the end of each cycle,
+                // so the service is not deferred there
+                if (activity) phase3(S, K, c, ej, t, acc);
+                else { pend = ej; has_pend = true; }
+            }
             busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
         if (activity) {
