@@ -31,6 +31,7 @@ enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4 
 #define HOLDER_NONE 0xFFFFFFFFu
 #define AGE_MAX     65535u   /* R32: field width of the deflection age */
 #define PEND_MAX    1023u    /* R32: field width of the pending-EV count */
+#define LIFE_MAX    ((1ull << 27) - 1)  /* R32: cycles a flit may stay in the network */
 
 typedef struct {
     int present;
@@ -534,6 +535,7 @@ static void phase2(orc_sim *s, uint32_t n)
     if (nf == 0) return;
     for (uint32_t i = 0; i < nf; ++i) {
         A[i].dst = F[i].dst; A[i].src = F[i].src; A[i].age = F[i].age; A[i].inj = F[i].inj;
+        if (s->t - F[i].inj > LIFE_MAX) fail(s, ORC_EOVERFLOW, "flit lifetime overflow");
     }
     if (arbitrate(s->W, s->H, n, s->cfg.prio, nf, A, port, defl) != 0) {
         fail(s, ORC_EASSERT, "more flits than ports at a router");

@@ -25,6 +25,7 @@ enum : uint32_t {
 enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8 };
 
 constexpr uint32_t AGE_MAX = 65535u;   // R32
+constexpr uint32_t LIFE_MAX = (1u << 27) - 1u;   // R32: flit lifetime t - inj
 constexpr uint32_t PEND_MAX = 1023u;   // R32
 constexpr uint32_t HOLDER_BITS = 22;   // loc entry = (holder+1) | pend << 22   (R36: 4 B)
 constexpr uint32_t HOLDER_MASK = (1u << HOLDER_BITS) - 1u;
@@ -143,6 +144,7 @@ struct Dev {
     uint32_t W, H, N, n0, nloc, row0, rows;
     uint32_t mode, prio, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
     uint32_t qcap, nb, seed_lo, seed_hi;
+    uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi
     uint32_t gen;                     // generation enabled (0 during drain)
     uint32_t has_script;
     // state

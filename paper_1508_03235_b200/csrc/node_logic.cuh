@@ -287,75 +287,79 @@ __device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx
 // ---------------------------------------------------------------------------
 // Phase 2: rank and port selection (PMDR P:L116)
 // ---------------------------------------------------------------------------
-// true if a ranks before b at cycle t (R1, R2)
-__device__ __forceinline__ bool ranks_before(uint32_t prio, const Flit &a, const Flit &b, uint32_t t32)
-{
-    if (prio == 0u) {
-        uint32_t aa = f_age(a), ab = f_age(b);
-        if (aa != ab) return aa > ab;
-    }
-    uint32_t la = t32 - a.z, lb = t32 - b.z;     // lifetimes: older = larger
-    if (la != lb) return la > lb;
-    return f_src(a) < f_src(b);
-}
-
 // The <= 5 router inputs (4 link slots + the injection slot) held in registers.
 struct Inputs {
     Flit f[5];
     uint32_t present;   // bit k: slot k holds a flit
 };
 
-// compare-exchange of slots I, J (I < J): afterwards slot I ranks before slot J;
-// empty slots sink to the end
-template <int I, int J>
-__device__ __forceinline__ void cex(Inputs &in, uint32_t prio, uint32_t t32)
+// Priority key of a flit at cycle t (R1, R2): a larger key ranks first.
+//   DEFLECT: age desc, then lifetime t-inj desc (= inj asc), then src asc
+//   OLDEST : lifetime desc, then src asc
+// Packed as age[48:64) | lifetime[21:48) | (2^21-1-src)[0:21); a lifetime of
+// 2^27 cycles or more is a field-width overflow (R32).
+__device__ __forceinline__ uint64_t prio_key(const Dev &S, const Flit &f, uint32_t t32)
 {
-    const bool pi = (in.present >> I) & 1u, pj = (in.present >> J) & 1u;
-    const bool sw = pj && (!pi || ranks_before(prio, in.f[J], in.f[I], t32));
-    if (sw) {
-        Flit tmp = in.f[I];
-        in.f[I] = in.f[J];
-        in.f[J] = tmp;
-        in.present = (in.present & ~((1u << I) | (1u << J))) | ((uint32_t)pj << I) | ((uint32_t)pi << J);
-    }
+    uint32_t life = t32 - f.z;
+    if (life > LIFE_MAX) { atomicOr(S.err, ERR_AGE); life = LIFE_MAX; }
+    uint64_t k = ((uint64_t)life << 21) | (NODE_MASK - f_src(f));
+    if (S.prio == 0u) k |= (uint64_t)f_age(f) << 48;
+    return k;
 }
 
-// Rank + port selection for the router of node c (R3-R6).
-// Output callback: Out(port, flit) stores a routed flit into the next-cycle slot.
+// dst -> (x, y) without a hardware divide: umulhi by ceil(2^32/W) is exact for
+// node ids < 2^21 (W <= 2048)
+__device__ __forceinline__ uint32_t row_of(const Dev &S, uint32_t n) { return __umulhi(n, S.wmagic); }
+
+// Rank + port selection for the router of node c (R3-R6):
+// flits are taken in priority order ("Priority Sort") by repeated
+// selection of the largest key; each takes the eject link (if at its
+// destination and still free), else its first free productive port (x before
+// y, PMDR), else the first free existing port in N,S,E,W with age+1.
+// Output callback Out(port, flit) stores a routed flit into its next-cycle slot.
+// Returns the mask of output ports taken.
 template <typename Out>
 __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs &in, uint64_t t, Acc &acc,
-                                      Flit &ej, bool &has_ej, Out &&out)
+                                          Flit &ej, bool &has_ej, Out &&out)
 {
     const uint32_t t32 = (uint32_t)t;
-    // "Priority Sort": optimal 9-comparator network for 5 inputs
-    cex<0, 1>(in, S.prio, t32); cex<3, 4>(in, S.prio, t32); cex<2, 4>(in, S.prio, t32);
-    cex<2, 3>(in, S.prio, t32); cex<1, 4>(in, S.prio, t32); cex<0, 3>(in, S.prio, t32);
-    cex<0, 2>(in, S.prio, t32); cex<1, 3>(in, S.prio, t32); cex<1, 2>(in, S.prio, t32);
-    uint32_t exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) |
-                     (c.x > 0 ? 8u : 0u);
-    uint32_t used = 0;
+    uint64_t key[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) key[k] = ((in.present >> k) & 1u) ? prio_key(S, in.f[k], t32) : 0ull;
+    const uint32_t exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) |
+                           (c.x > 0 ? 8u : 0u);
+    uint32_t used = 0, left = in.present;
     has_ej = false;
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        if (!((in.present >> i) & 1u)) break;
-        Flit f = in.f[i];
-        uint32_t dst = f_dst(f);
-        if (dst == c.n && !has_ej) { ej = f; has_ej = true; continue; }
+    for (int r = 0; r < 5; ++r) {
+        if (!left) break;
+        // the highest-priority remaining flit (keys of present flits are > 0)
+        int bi = 0;
+        uint64_t bk = 0;
+        Flit f = in.f[0];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            if (((left >> k) & 1u) && key[k] > bk) { bk = key[k]; bi = k; f = in.f[k]; }
+        }
+        left &= ~(1u << bi);
+        const uint32_t dst = f_dst(f);
+        if (dst == c.n) {
+            if (!has_ej) { ej = f; has_ej = true; continue; }
+        }
         int p = -1;
         if (dst != c.n) {
-            uint32_t dy = dst / S.W, dx = dst - dy * S.W;
+            const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
             if (dx != c.x) {
-                uint32_t xp = dx > c.x ? PE : PW;
+                const uint32_t xp = dx > c.x ? PE : PW;
                 if (!(used & (1u << xp))) p = (int)xp;
             }
             if (p < 0 && dy != c.y) {
-                uint32_t yp = dy > c.y ? PS : PN;
+                const uint32_t yp = dy > c.y ? PS : PN;
                 if (!(used & (1u << yp))) p = (int)yp;
             }
         }
         if (p < 0) {
-            uint32_t freep = exist & ~used;            // first free existing port in N,S,E,W (R5)
-            p = (int)(__ffs(freep) - 1);
+            p = (int)(__ffs(exist & ~used) - 1);     // first free existing port in N,S,E,W (R5)
             uint32_t a = f_age(f) + 1u;
             if (a > AGE_MAX) { atomicOr(S.err, ERR_AGE); a = AGE_MAX; }
             f_set_age(f, a);
@@ -365,7 +369,7 @@ __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs
         ++acc.hops;
         out((uint32_t)p, f);
     }
-    return used;   // output ports taken
+    return used;
 }
 
 // ---------------------------------------------------------------------------

@@ -173,6 +173,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     D.seed_lo = (uint32_t)cfg->seed;
     D.seed_hi = (uint32_t)(cfg->seed >> 32);
     D.gen = 1;
+    D.wmagic = (uint32_t)(((1ull << 32) + D.W - 1) / D.W);
     const size_t n = D.nloc;
 
     for (int b = 0; b < 2; ++b) {

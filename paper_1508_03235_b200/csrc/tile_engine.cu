@@ -40,6 +40,12 @@ __device__ __forceinline__ unsigned long long llw(uint32_t stamp, uint32_t data)
     return ((unsigned long long)data << 32) | stamp;
 }
 
+// a[p] for a runtime p without indexing a local array (keeps a[] in registers)
+__device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t p)
+{
+    return p == 0u ? a[0] : p == 1u ? a[1] : p == 2u ? a[2] : a[3];
+}
+
 struct TileShape {
     uint32_t x0, y0, tw, th, tn;
 };
@@ -128,6 +134,24 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     }
     __syncthreads();
 
+    // LL word offsets (parity 0) of this node's boundary input slots and of the
+    // neighbours' slots its boundary output ports feed; parity 1 adds pstride
+    const uint32_t pstride = 16u * S.nloc;
+    uint32_t inw[4], outw[4], outi[4];
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d) {
+        inw[d] = (uint32_t)ll_index(S, 0, d, c.l, 0);
+        uint32_t m = c.l, mi = i;
+        switch (d) {
+        case PN: m = c.l - S.W; mi = i - T.tw; break;
+        case PS: m = c.l + S.W; mi = i + T.tw; break;
+        case PE: m = c.l + 1u; mi = i + 1u; break;
+        default: m = c.l - 1u; mi = i - 1u; break;
+        }
+        outw[d] = ((ext >> d) & 1u) ? (uint32_t)ll_index(S, 0, d ^ 1u, m, 0) : 0u;
+        outi[d] = mi;
+    }
+
     Sink K{scnt, shist};
     Acc acc = {0, 0, 0, 0};
     Flit pend;
@@ -142,9 +166,11 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
             // issue the boundary polls first: their latency overlaps the
             // deferred service and Phase 1
             unsigned long long xw[4] = {0, 0, 0, 0};
+            unsigned long long *const llp = S.ll + (size_t)pb * pstride;     // this cycle's inputs
+            unsigned long long *const lln = S.ll + (size_t)nb1 * pstride;    // next cycle's inputs
 #pragma unroll
             for (uint32_t d = 0; d < 4; ++d)
-                if ((ext >> d) & 1u) xw[d] = ld_relaxed_u64(&S.ll[ll_index(S, pb, d, c.l, 0)]);
+                if ((ext >> d) & 1u) xw[d] = ld_relaxed_u64(llp + inw[d]);
 
             // deferred Phase 3 of cycle t-1
             if (has_pend) { phase3(S, K, c, pend, t - 1, acc); has_pend = false; }
@@ -171,7 +197,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
 #pragma unroll
             for (uint32_t d = 0; d < 4; ++d) {
                 if (!((ext >> d) & 1u)) continue;
-                const unsigned long long *slot = &S.ll[ll_index(S, pb, d, c.l, 0)];
+                const unsigned long long *slot = llp + inw[d];
                 uint32_t spins = 0;
                 unsigned long long w = xw[d];
                 while ((uint32_t)w != st32) {
@@ -202,45 +228,23 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
                 used = route(S, c, in, t, acc, ej, has_ej, [&](uint32_t p, const Flit &f) {
                     const uint32_t slot = p ^ 1u;   // opp(p): N<->S (0,1), E<->W (2,3)
                     if ((ext >> p) & 1u) {
-                        uint32_t m;
-                        switch (p) {
-                        case PN: m = c.l - S.W; break;
-                        case PS: m = c.l + S.W; break;
-                        case PE: m = c.l + 1u; break;
-                        default: m = c.l - 1u; break;
-                        }
-                        unsigned long long *o = &S.ll[ll_index(S, nb1, slot, m, 0)];
+                        unsigned long long *o = lln + pick4(outw, p);
                         st_relaxed_u64(o + 1, llw(st32n, f.y));
                         st_relaxed_u64(o + 2, llw(st32n, f.z));
                         st_relaxed_u64(o + 3, llw(st32n, f.w));
                         st_relaxed_u64(o, llw(st32n, f.x));
                     } else {
-                        uint32_t mi;
-                        switch (p) {
-                        case PN: mi = i - T.tw; break;
-                        case PS: mi = i + T.tw; break;
-                        case PE: mi = i + 1u; break;
-                        default: mi = i - 1u; break;
-                        }
+                        const uint32_t mi = pick4(outi, p);
                         sflit[(nb1 * 4u + slot) * tpad + mi] = make_uint4(f.x, f.y, f.z, f.w);
                         reinterpret_cast<uint8_t *>(sflag + nb1 * tpad + mi)[slot] = st1;
                     }
                 });
             }
             // boundary ports without a flit carry an explicit EMPTY every cycle
-            uint32_t idle_ext = ext & ~used;
-            while (idle_ext) {
-                const uint32_t p = __ffs(idle_ext) - 1u;
-                idle_ext &= idle_ext - 1u;
-                uint32_t m;
-                switch (p) {
-                case PN: m = c.l - S.W; break;
-                case PS: m = c.l + S.W; break;
-                case PE: m = c.l + 1u; break;
-                default: m = c.l - 1u; break;
-                }
-                st_relaxed_u64(&S.ll[ll_index(S, nb1, p ^ 1u, m, 0)], llw(st32n, LL_EMPTY));
-            }
+            const uint32_t idle_ext = ext & ~used;
+#pragma unroll
+            for (uint32_t p = 0; p < 4; ++p)
+                if ((idle_ext >> p) & 1u) st_relaxed_u64(lln + outw[p], llw(st32n, LL_EMPTY));
             if (has_ej) {
                 // while draining, quiescence is judged at the end of each cycle,
                 // so the service is not deferred there
