@@ -126,7 +126,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
         for (uint32_t d = 0; d < 4; ++d) {
             if (!((ext >> d) & 1u) && ((fl >> (8u * d)) & 0xFFu) == st0) {
                 sflit[(b0 * 4u + d) * tpad + i] = S.flit[b0][(size_t)d * S.nloc + c.l];
-                sfl |= 1u << (8u * d);
+                sfl |= (uint32_t)st0 << (8u * d);
             }
         }
         sflag[b0 * tpad + i] = sfl;

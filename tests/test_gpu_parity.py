@@ -199,3 +199,19 @@ def test_tiled_odd_tilings(w, h):
     cfg = W.make(mesh_w=w, mesh_h=h, mode=W.MODE_UR, lam=0.2)
     g, o = both(cfg, 1500, nb.ENGINE_TILED)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
+def test_launch_boundaries(engine, mode):
+    """State carried across many short launches (links spilled / reloaded,
+    deferred services finished) equals one long run and the oracle."""
+    cfg = (W.make(mesh_w=16, mesh_h=16, mode=mode, lam=0.3) if mode == W.MODE_UR
+           else W.lspd(24, 20, lam=0.2))
+    g, o = both(cfg, None, engine, split=[1, 1, 2, 3, 5, 8, 13, 21, 34, 55, 89, 144, 233])
+    assert_same(g, o)
+    g.drain(7)
+    o.drain(7)
+    g.run(100)
+    o.run(100)
+    assert_same(g, o)
