@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, u
     Sink K{scnt, shist};
     Acc acc = {0, 0, 0, 0};
     __shared__ int s_abort;
-    if (threadIdx.x == 0) s_abort = 0;
+    __shared__ uint32_t s_busy[2];
+    if (threadIdx.x == 0) { s_abort = 0; s_busy[0] = s_busy[1] = 0u; }
     __syncthreads();
 
     for (uint32_t c = 0; c < ncyc; ++c) {
@@ -109,12 +110,11 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, u
         bool busy = false;
         for (uint32_t l = lo_node + threadIdx.x; l < hi_node; l += blockDim.x)
             busy |= node_step_global<MODE>(S, K, l, t, acc);
-        if (activity) {
-            if (__syncthreads_or(busy) && threadIdx.x == 0) atomicAdd(&activity[c], 1u);
-        } else {
-            __syncthreads();
-        }
+        // full BAR.SYNC (see tile_engine.cu); busy nodes stamp a per-parity word
+        if (activity && busy) s_busy[c & 1u] = c + 1u;
+        __syncthreads();
         if (threadIdx.x == 0) {
+            if (activity && s_busy[c & 1u] == c + 1u) atomicAdd(&activity[c], 1u);
             __threadfence();
             st_release_u32(&progress[b], pbase + c + 1u);
         }

@@ -81,6 +81,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     unsigned int *scnt = sflag + 2u * tpad;
     unsigned int *shist = smem_hist ? scnt + NCOUNTERS : nullptr;
     __shared__ int s_abort;
+    __shared__ uint32_t s_busy[2];
 
     const uint32_t i = threadIdx.x;
     const TileShape T = tile_shape(S, blockIdx.x);
@@ -89,7 +90,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     {
         const uint32_t nsm = NCOUNTERS + (smem_hist ? 3u * S.nb : 0u);
         for (uint32_t k = i; k < nsm; k += blockDim.x) scnt[k] = 0u;
-        if (i == 0) s_abort = 0;
+        if (i == 0) { s_abort = 0; s_busy[0] = s_busy[1] = 0u; }
     }
 
     // ---- node registers (persist for the whole launch)
@@ -253,11 +254,13 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
             }
             busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
-        if (activity) {
-            if (__syncthreads_or(busy) && i == 0) atomicAdd(&activity[cc], 1u);
-        } else {
-            __syncthreads();
-        }
+        // The cycle barrier must be a full BAR.SYNC: it orders the shared-memory
+        // link stores of this cycle before next cycle's loads.  (A reducing
+        // barrier, __syncthreads_or, measurably did not on sm_100a.)  Busy
+        // nodes instead stamp a per-parity shared word with the cycle index.
+        if (activity && busy) s_busy[cc & 1u] = cc + 1u;
+        __syncthreads();
+        if (activity && i == 0 && s_busy[cc & 1u] == cc + 1u) atomicAdd(&activity[cc], 1u);
         if (s_abort) break;
     }
 

@@ -215,3 +215,14 @@ def test_launch_boundaries(engine, mode):
     g.run(100)
     o.run(100)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c3_drain_window(engine):
+    """Drain (generation off) at the bench size, checked against the oracle
+    mid-drain: multi-warp tiles exchange links through shared memory."""
+    cfg = W.c3()
+    g, o = both(cfg, 1200, engine)
+    for k in (37, 200):
+        assert g.drain(k) == o.drain(k)
+        assert_same(g, o)

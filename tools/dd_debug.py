@@ -3,17 +3,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1508_03235_b200 as pkg
 from paper_1508_03235_b200 import workloads as W
 from oracle import Oracle
-cfg = W.make(mesh_w=16, mesh_h=16, mode=0, lam=0.3)
-for seq in ([("run", 305)], [("run", 300), ("run", 5)], [("run", 1), ("run", 1)], [("run", 2), ("run", 2), ("run", 2)], [("run", 300), ("drain", 5)]):
-    s = pkg.NocSim(cfg, engine=3)
-    o = Oracle(cfg)
-    out = []
-    for op, arg in seq:
-        if op == "run":
-            s.run(arg); o.run(arg)
-        else:
-            s.drain(arg); o.drain(arg)
-        gs, os_ = s.stats()[0], o.stats()[0]
-        out.append((op, arg, s.state_hash() == o.state_hash(), {k: (gs[k], os_[k]) for k in gs if gs[k] != os_[k]}))
-    print(s.info(), flush=True)
-    print(out, flush=True)
+cfg = W.c3()
+o = Oracle(cfg); o.run(1500)
+sims = {e: pkg.NocSim(cfg, engine=e) for e in (1, 2, 3)}
+for s in sims.values(): s.run(1500)
+print("run", {e: s.state_hash() == o.state_hash() for e, s in sims.items()}, flush=True)
+for k in (10, 50, 200):
+    ro = o.drain(k)
+    so = o.stats()[0]
+    for e, s in sims.items():
+        r = s.drain(k); ss = s.stats()[0]
+        print(k, e, r, ro, s.state_hash() == o.state_hash(), {kk: (ss[kk], so[kk]) for kk in ss if ss[kk] != so[kk]}, flush=True)
