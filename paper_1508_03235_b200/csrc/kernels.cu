@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_step(Dev S, uint64_t t, uint32_t *activ
 {
     uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
     Acc acc = {0, 0, 0, 0};
-    Sink K{nullptr, nullptr};
+    Sink K{nullptr, nullptr, true};
     bool busy = false;
     if (l < S.nloc) busy = node_step_global<MODE>(S, K, l, t, acc);
     flush_acc(S, acc, nullptr);
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, u
     const uint32_t first = lo_node >= S.W ? (lo_node - S.W) / nodes_per_cta : 0u;
     const uint32_t lastn = min(S.nloc - 1u, hi_node - 1u + S.W);
     const uint32_t last = min(G - 1u, lastn / nodes_per_cta);
-    Sink K{scnt, shist};
+    Sink K{scnt, shist, true};
     Acc acc = {0, 0, 0, 0};
     __shared__ int s_abort;
     __shared__ uint32_t s_busy[2];

@@ -14,16 +14,22 @@ namespace noc {
 
 // Statistic sink.  Rare counters / histogram bins go to shared memory (u32)
 // when the kernel provides it, else straight to global u64 atomics.
+// When a node's state is replicated across several lanes (TILED engine), every
+// lane executes the same model code and performs the same (idempotent) global
+// stores; only the lead lane (on = true) counts.
 struct Sink {
     unsigned int *scnt;    // [NCOUNTERS] or nullptr
     unsigned int *shist;   // [3][nb] or nullptr
+    bool on;
     __device__ __forceinline__ void cnt(const Dev &S, uint32_t i, uint32_t v = 1u) const
     {
+        if (!on) return;
         if (scnt) atomicAdd(&scnt[i], v);
         else atomicAdd(&S.cnt[i], (unsigned long long)v);
     }
     __device__ __forceinline__ void hist(const Dev &S, uint32_t h, uint32_t v) const
     {
+        if (!on) return;
         uint32_t b = v < S.nb - 1u ? v : S.nb - 1u;
         if (shist) atomicAdd(&shist[h * S.nb + b], 1u);
         else atomicAdd(&S.hist[(size_t)h * S.nb + b], 1ull);
@@ -377,7 +383,7 @@ __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs
 // ---------------------------------------------------------------------------
 static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Flit &f, uint64_t t, Acc &acc)
 {
-    ++acc.ejected;
+    if (K.on) ++acc.ejected;
     K.hist(S, 0, (uint32_t)t - f.z);
     K.hist(S, 1, f_age(f));
     switch (f_kind(f)) {
