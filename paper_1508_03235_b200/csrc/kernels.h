@@ -5,9 +5,8 @@
 namespace noc {
 
 constexpr uint32_t PERSIST_BLOCK = 256;
-constexpr uint32_t TILE_MAX_NODES = 160;                  // 4 lanes per node
-constexpr uint32_t TILE_BLOCK_MAX = 4 * TILE_MAX_NODES;   // threads per CTA
-constexpr uint32_t TILE_MIN_BLOCKS = 2;                   // co-resident CTAs per SM
+constexpr uint32_t TILE_BLOCK_MAX = 512;                  // nodes (= threads) per CTA
+constexpr uint32_t TILE_MIN_BLOCKS = 1;                   // co-resident CTAs per SM
 
 // TILED engine (tile_engine.cu): configure picks the tiling (sets S.TX, S.TY)
 cudaError_t tiled_configure(Dev &S, int device, uint32_t *grid, uint32_t *tpad, uint32_t *smem_hist);

@@ -329,6 +329,39 @@ __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs
                                           Flit &ej, bool &has_ej, Out &&out)
 {
     const uint32_t t32 = (uint32_t)t;
+    // Fast path: if the flits' first choices (eject at the destination, else
+    // the x-port if dx != 0, else the y-port) are pairwise distinct, the
+    // greedy gives every flit its first choice whatever the ranking, and
+    // nothing is deflected.  (Lifetimes are still checked, R32.)
+    {
+        uint32_t fc[5], seen = 0;
+        bool coll = false;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            fc[k] = PX;
+            if ((in.present >> k) & 1u) {
+                if (t32 - in.f[k].z > LIFE_MAX) atomicOr(S.err, ERR_AGE);
+                const uint32_t dst = f_dst(in.f[k]);
+                if (dst != c.n) {
+                    const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
+                    fc[k] = dx != c.x ? (dx > c.x ? PE : PW) : (dy > c.y ? PS : PN);
+                }
+                coll |= (seen >> fc[k]) & 1u;
+                seen |= 1u << fc[k];
+            }
+        }
+        if (!coll) {
+            has_ej = false;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                if (!((in.present >> k) & 1u)) continue;
+                if (fc[k] == PX) { ej = in.f[k]; has_ej = true; continue; }
+                ++acc.hops;
+                out(fc[k], in.f[k]);
+            }
+            return seen & 15u;
+        }
+    }
     uint64_t key[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) key[k] = ((in.present >> k) & 1u) ? prio_key(S, in.f[k], t32) : 0ull;
