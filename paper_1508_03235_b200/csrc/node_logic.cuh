@@ -49,6 +49,9 @@ struct NodeCtx {
     uint4 cold;
     uint2 head;          // cached head packet of the send FIFO (valid iff head_ok)
     bool head_ok;
+    // generation draw computed one cycle ahead (valid iff nd_ok and nd_t == t)
+    bool nd_ok, nd_fire;
+    uint32_t nd_t, nd_val;
     bool q_dirty, hot_dirty, cold_dirty, cold_loaded;
     bool busy_flit;      // sent a flit this cycle (drain detection)
 };
@@ -239,6 +242,78 @@ __device__ __forceinline__ bool script_next(const Dev &S, const NodeCtx &c, uint
 // ---------------------------------------------------------------------------
 // Phase 1
 // ---------------------------------------------------------------------------
+// The Philox draw of node n for cycle t (R25): fire flag and value (UR: probe
+// destination; LSPD: block tag, DESIGN 3.3).
+__device__ __forceinline__ bool draw(const Dev &S, const NodeCtx &c, uint64_t t, uint32_t &val)
+{
+    uint32_t r[4];
+    philox4x32_10(S.seed_lo, S.seed_hi, c.n, (uint32_t)t, (uint32_t)(t >> 32), 0u, r);
+    if (r[0] >= S.thr_inj) return false;
+    if (S.mode == 0u) {
+        uint32_t d = mulhi32(r[1], S.N - 1u);
+        val = d + (d >= c.n);
+    } else if (r[1] < S.thr_priv) {
+        val = c.n * S.tpn + mulhi32(r[2], S.priv);
+    } else {
+        val = mulhi32(r[2], S.N) * S.tpn + S.priv + mulhi32(r[3], S.tpn - S.priv);
+    }
+    return true;
+}
+
+// The draw for cycle t: the one computed ahead if any, else computed now.
+__device__ __forceinline__ bool draw_now(const Dev &S, NodeCtx &c, uint64_t t, uint32_t &val)
+{
+    if (c.nd_ok && c.nd_t == (uint32_t)t) {
+        c.nd_ok = false;
+        val = c.nd_val;
+        return c.nd_fire;
+    }
+    return draw(S, c, t, val);
+}
+
+__device__ __forceinline__ void prefetch_l1(const void *p)
+{
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// L2-slice set of tag T of node c (first line)
+__device__ __forceinline__ const uint4 *set_ptr(const Dev &S, const NodeCtx &c, uint32_t T)
+{
+    return S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways;
+}
+
+// End of cycle t (TILED engine): compute the draw of cycle t+1 ahead when the
+// core will draw then, and prefetch the L2-slice set Phase 1 will probe at t+1
+// (an access start or a memory fill), so the lookup hits L1.  Pure
+// prefetching: the model is unchanged.
+__device__ __forceinline__ void predraw(const Dev &S, NodeCtx &c, uint64_t t1)
+{
+    if (!S.gen || S.has_script) return;
+    if (S.mode == 0u) {
+        c.nd_fire = draw(S, c, t1, c.nd_val);
+        c.nd_t = (uint32_t)t1;
+        c.nd_ok = true;
+        return;
+    }
+    const uint32_t mode = core_mode(c.hot);
+    const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t1) & 0x1FFFFFFFu) == 0u);
+    if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
+    if (mode == MIDLE || expiring) {
+        c.nd_fire = draw(S, c, t1, c.nd_val);
+        c.nd_t = (uint32_t)t1;
+        c.nd_ok = true;
+        if (c.nd_fire) prefetch_l1(set_ptr(S, c, c.nd_val));
+    }
+}
+
+// At ejection: prefetch what the (deferred) service of flit f will read.
+__device__ __forceinline__ void prefetch_service(const Dev &S, const NodeCtx &c, const Flit &f)
+{
+    const uint32_t k = f_kind(f);
+    if (k == KDA || k == KEV) prefetch_l1(&S.loc[loc_index(S, f.w)]);
+    else if (k == KRQ) prefetch_l1(set_ptr(S, c, f.w));
+}
+
 __device__ __forceinline__ void phase1_ur(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
 {
     if (!S.gen) return;
@@ -247,13 +322,7 @@ __device__ __forceinline__ void phase1_ur(const Dev &S, const Sink &K, NodeCtx &
     if (S.has_script && script_next(S, c, t, v)) {
         fire = true; dst = v;
     } else {
-        uint32_t r[4];
-        philox4x32_10(S.seed_lo, S.seed_hi, c.n, (uint32_t)t, (uint32_t)(t >> 32), 0u, r);
-        if (r[0] < S.thr_inj) {
-            uint32_t d = mulhi32(r[1], S.N - 1u);
-            d += (d >= c.n);
-            fire = true; dst = d;
-        }
+        fire = draw_now(S, c, t, dst);
     }
     if (fire) {
         K.cnt(S, C_GENERATED);
@@ -278,13 +347,7 @@ __device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx
         if (S.has_script && script_next(S, c, t, v)) {
             fire = true; T = v;
         } else {
-            uint32_t r[4];
-            philox4x32_10(S.seed_lo, S.seed_hi, c.n, (uint32_t)t, (uint32_t)(t >> 32), 0u, r);
-            if (r[0] < S.thr_inj) {
-                fire = true;
-                if (r[1] < S.thr_priv) T = c.n * S.tpn + mulhi32(r[2], S.priv);
-                else T = mulhi32(r[2], S.N) * S.tpn + S.priv + mulhi32(r[3], S.tpn - S.priv);
-            }
+            fire = draw_now(S, c, t, T);
         }
         if (fire) start_access(S, K, c, T, t);
     }
@@ -515,6 +578,7 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
     c.qctl = S.fifo_ctl[l];
     c.hot = MODE == 1u ? S.core_hot[l] : 0u;
     c.head_ok = false;
+    c.nd_ok = false;
     c.q_dirty = c.hot_dirty = c.cold_dirty = c.cold_loaded = false;
     c.busy_flit = false;
 

@@ -42,6 +42,19 @@ __device__ __forceinline__ unsigned long long llw(uint32_t stamp, uint32_t data)
     return ((unsigned long long)data << 32) | stamp;
 }
 
+// 16-byte relaxed accesses (two LL words).  Each 64-bit word carries its own
+// stamp, so the receiver validates every word; no 128-bit atomicity is assumed.
+__device__ __forceinline__ void ld_relaxed_x2(const unsigned long long *p, unsigned long long &a,
+                                              unsigned long long &b)
+{
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_x2(unsigned long long *p, unsigned long long a, unsigned long long b)
+{
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
 // a[p] for a runtime p without indexing a local array (keeps a[] in registers)
 __device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t p)
 {
@@ -103,6 +116,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     c.n = c.y * S.W + c.x;
     c.l = c.n - S.n0;
     c.head_ok = false;
+    c.nd_ok = false;
     c.cold_loaded = true;
     c.q_dirty = c.hot_dirty = c.cold_dirty = false;
     c.busy_flit = false;
@@ -171,11 +185,15 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
         if (active) {
             unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
             unsigned long long *const lln = S.ll + (size_t)nb1 * pstride;  // next cycle's
-            // issue the boundary polls first
-            unsigned long long xw[4] = {0, 0, 0, 0};
+            // issue the boundary polls first (all four words of each slot)
+            unsigned long long xa[4] = {0, 0, 0, 0}, xb[4] = {0, 0, 0, 0}, xc[4] = {0, 0, 0, 0},
+                               xd[4] = {0, 0, 0, 0};
 #pragma unroll
             for (uint32_t d = 0; d < 4; ++d)
-                if ((ext >> d) & 1u) xw[d] = ld_relaxed_u64(llp + inw[d]);
+                if ((ext >> d) & 1u) {
+                    ld_relaxed_x2(llp + inw[d], xa[d], xb[d]);
+                    ld_relaxed_x2(llp + inw[d] + 2, xc[d], xd[d]);
+                }
 
             // deferred Phase 3 of cycle t-1
             if (has_pend) { phase3(S, K, c, pend, t - 1, acc); has_pend = false; }
@@ -202,21 +220,18 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
                 if (!((ext >> d) & 1u)) continue;
                 const unsigned long long *slot = llp + inw[d];
                 uint32_t spins = 0;
-                unsigned long long w = xw[d];
-                while ((uint32_t)w != st) {
+                unsigned long long w0 = xa[d], w1 = xb[d], w2 = xc[d], w3 = xd[d];
+                // the slot is complete when word 0 carries this cycle's stamp
+                // and, for a flit (not EMPTY), so do words 1..3
+                while ((uint32_t)w0 != st ||
+                       ((uint32_t)(w0 >> 32) != LL_EMPTY &&
+                        ((uint32_t)w1 != st || (uint32_t)w2 != st || (uint32_t)w3 != st))) {
                     if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
-                    w = ld_relaxed_u64(slot);
+                    ld_relaxed_x2(slot, w0, w1);
+                    ld_relaxed_x2(slot + 2, w2, w3);
                 }
-                const uint32_t x = (uint32_t)(w >> 32);
-                if ((uint32_t)w == st && x != LL_EMPTY) {
-                    unsigned long long w1 = ld_relaxed_u64(slot + 1), w2 = ld_relaxed_u64(slot + 2),
-                                       w3 = ld_relaxed_u64(slot + 3);
-                    while ((uint32_t)w1 != st || (uint32_t)w2 != st || (uint32_t)w3 != st) {
-                        if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
-                        if ((uint32_t)w1 != st) w1 = ld_relaxed_u64(slot + 1);
-                        if ((uint32_t)w2 != st) w2 = ld_relaxed_u64(slot + 2);
-                        if ((uint32_t)w3 != st) w3 = ld_relaxed_u64(slot + 3);
-                    }
+                const uint32_t x = (uint32_t)(w0 >> 32);
+                if ((uint32_t)w0 == st && x != LL_EMPTY) {
                     in.f[d] = Flit{x, (uint32_t)(w1 >> 32), (uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32)};
                     in.present |= 1u << d;
                 }
@@ -231,10 +246,8 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
                     const uint32_t slot = p ^ 1u;   // opp(p): N<->S (0,1), E<->W (2,3)
                     if ((ext >> p) & 1u) {
                         unsigned long long *o = lln + pick4(outw, p);
-                        st_relaxed_u64(o + 1, llw(stn, f.y));
-                        st_relaxed_u64(o + 2, llw(stn, f.z));
-                        st_relaxed_u64(o + 3, llw(stn, f.w));
-                        st_relaxed_u64(o, llw(stn, f.x));
+                        st_relaxed_x2(o + 2, llw(stn, f.z), llw(stn, f.w));
+                        st_relaxed_x2(o, llw(stn, f.x), llw(stn, f.y));
                     } else {
                         const uint32_t so = (nb1 * 4u + slot) * np + pick4(outi, p);
                         sflit[so] = make_uint4(f.x, f.y, f.z, f.w);
@@ -251,9 +264,11 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
                 // while draining, quiescence is judged at the end of each cycle,
                 // so the service is not deferred there
                 if (activity) phase3(S, K, c, ej, t, acc);
-                else { pend = ej; has_pend = true; }
+                else { pend = ej; has_pend = true; if (MODE == 1u) prefetch_service(S, c, ej); }
             }
             busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
+            // the generation draw of cycle t+1, off the critical path
+            predraw(S, c, t + 1);
         }
         // The cycle barrier is a full BAR.SYNC: it orders this cycle's shared-
         // memory link stores before the next cycle's loads (a reducing barrier,
