@@ -288,13 +288,9 @@ __device__ __forceinline__ const uint4 *set_ptr(const Dev &S, const NodeCtx &c, 
 // prefetching: the model is unchanged.
 __device__ __forceinline__ void predraw(const Dev &S, NodeCtx &c, uint64_t t1)
 {
-    if (!S.gen || S.has_script) return;
-    if (S.mode == 0u) {
-        c.nd_fire = draw(S, c, t1, c.nd_val);
-        c.nd_t = (uint32_t)t1;
-        c.nd_ok = true;
-        return;
-    }
+    // UR draws every cycle: computing it here would only delay the next
+    // boundary poll, so only the (rarer) LSPD draws are taken ahead
+    if (!S.gen || S.has_script || S.mode == 0u) return;
     const uint32_t mode = core_mode(c.hot);
     const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t1) & 0x1FFFFFFFu) == 0u);
     if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
