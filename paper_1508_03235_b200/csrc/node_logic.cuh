@@ -383,15 +383,30 @@ __device__ __forceinline__ uint32_t row_of(const Dev &S, uint32_t n) { return __
 // y, PMDR), else the first free existing port in N,S,E,W with age+1.
 // Output callback Out(port, flit) stores a routed flit into its next-cycle slot.
 // Returns the mask of output ports taken.
+// First choice of flit f at node c (eject at the destination, else the x-port
+// if dx != 0, else the y-port; PMDR P:L116), with the lifetime check (R32).
+__device__ __forceinline__ uint32_t first_choice(const Dev &S, const NodeCtx &c, const Flit &f, uint32_t t32)
+{
+    if (t32 - f.z > LIFE_MAX) atomicOr(S.err, ERR_AGE);
+    const uint32_t dst = f_dst(f);
+    if (dst == c.n) return PX;
+    const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
+    return dx != c.x ? (dx > c.x ? PE : PW) : (dy > c.y ? PS : PN);
+}
+
+// The general case: full ranking + greedy (see route()).
+template <typename Out>
+__device__ __forceinline__ uint32_t route_select(const Dev &S, const NodeCtx &c, Inputs &in, uint64_t t, Acc &acc,
+                                                 Flit &ej, bool &has_ej, Out &&out);
+
 template <typename Out>
 __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs &in, uint64_t t, Acc &acc,
                                           Flit &ej, bool &has_ej, Out &&out)
 {
     const uint32_t t32 = (uint32_t)t;
-    // Fast path: if the flits' first choices (eject at the destination, else
-    // the x-port if dx != 0, else the y-port) are pairwise distinct, the
-    // greedy gives every flit its first choice whatever the ranking, and
-    // nothing is deflected.  (Lifetimes are still checked, R32.)
+    // Fast path: if the flits' first choices are pairwise distinct, the greedy
+    // gives every flit its first choice whatever the ranking, and nothing is
+    // deflected.
     {
         uint32_t fc[5], seen = 0;
         bool coll = false;
@@ -399,12 +414,7 @@ __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs
         for (int k = 0; k < 5; ++k) {
             fc[k] = PX;
             if ((in.present >> k) & 1u) {
-                if (t32 - in.f[k].z > LIFE_MAX) atomicOr(S.err, ERR_AGE);
-                const uint32_t dst = f_dst(in.f[k]);
-                if (dst != c.n) {
-                    const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
-                    fc[k] = dx != c.x ? (dx > c.x ? PE : PW) : (dy > c.y ? PS : PN);
-                }
+                fc[k] = first_choice(S, c, in.f[k], t32);
                 coll |= (seen >> fc[k]) & 1u;
                 seen |= 1u << fc[k];
             }
@@ -421,6 +431,14 @@ __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs
             return seen & 15u;
         }
     }
+    return route_select(S, c, in, t, acc, ej, has_ej, out);
+}
+
+template <typename Out>
+__device__ __forceinline__ uint32_t route_select(const Dev &S, const NodeCtx &c, Inputs &in, uint64_t t, Acc &acc,
+                                                 Flit &ej, bool &has_ej, Out &&out)
+{
+    const uint32_t t32 = (uint32_t)t;
     uint64_t key[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) key[k] = ((in.present >> k) & 1u) ? prio_key(S, in.f[k], t32) : 0ull;
@@ -535,18 +553,18 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
 // Injection (R7, R8): one flit of the head packet per cycle, only
 // if fewer flits than ports arrived.  The injected flit takes slot 4.  When the
 // head packet is popped, the next head is fetched (used at t+1 at the earliest).
-__device__ __forceinline__ void inject(const Dev &S, NodeCtx &c, Inputs &in, uint64_t t, Acc &acc)
+__device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t npresent, uint64_t t, Acc &acc,
+                                            Flit &out)
 {
     const uint32_t deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
     const uint32_t qn = q_count(c.qctl);
-    if (qn == 0u || (uint32_t)__popc(in.present) >= deg) return;
+    if (qn == 0u || npresent >= deg) return false;
     const uint32_t h = q_head(c.qctl);
     uint32_t nx = q_next(c.qctl);
     if (!c.head_ok) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h]; c.head_ok = true; }
     const uint2 p = c.head;
     const uint32_t nfl = (p.x >> 24) & 15u;
-    in.f[4] = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
-    in.present |= 16u;
+    out = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
     ++acc.injected;
     ++nx;
     if (nx == nfl) {
@@ -558,6 +576,12 @@ __device__ __forceinline__ void inject(const Dev &S, NodeCtx &c, Inputs &in, uin
         c.qctl = q_make(h, qn, nx);
     }
     c.q_dirty = true;
+    return true;
+}
+
+__device__ __forceinline__ void inject(const Dev &S, NodeCtx &c, Inputs &in, uint64_t t, Acc &acc)
+{
+    if (inject_flit(S, c, (uint32_t)__popc(in.present), t, acc, in.f[4])) in.present |= 16u;
 }
 
 // The whole node step of cycle t with links in global memory (SoA).

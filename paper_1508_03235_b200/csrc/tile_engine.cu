@@ -80,9 +80,39 @@ __device__ __forceinline__ TileShape tile_shape(const Dev &S, uint32_t b)
     return T;
 }
 
+// Thread <-> node mapping inside a tile: the interior nodes (no boundary port)
+// take the first threads/warps, the boundary ring the last ones, so the warps
+// of interior nodes never execute (or wait in) the boundary-exchange code.
+__device__ __forceinline__ void tile_pos(const TileShape &T, uint32_t i, uint32_t &lx, uint32_t &ly)
+{
+    if (T.tw < 3 || T.th < 3) { lx = i % T.tw; ly = i / T.tw; return; }
+    const uint32_t iw = T.tw - 2, ic = iw * (T.th - 2);
+    if (i < ic) { lx = 1 + i % iw; ly = 1 + i / iw; return; }
+    uint32_t j = i - ic;
+    if (j < T.tw) { lx = j; ly = 0; return; }
+    j -= T.tw;
+    if (j < T.tw) { lx = j; ly = T.th - 1; return; }
+    j -= T.tw;
+    if (j < T.th - 2) { lx = 0; ly = 1 + j; return; }
+    j -= T.th - 2;
+    lx = T.tw - 1; ly = 1 + j;
+}
+
+__device__ __forceinline__ uint32_t tile_slot(const TileShape &T, uint32_t lx, uint32_t ly)
+{
+    if (T.tw < 3 || T.th < 3) return ly * T.tw + lx;
+    const uint32_t iw = T.tw - 2, ic = iw * (T.th - 2);
+    if (lx >= 1 && lx + 1 < T.tw && ly >= 1 && ly + 1 < T.th) return (ly - 1) * iw + (lx - 1);
+    if (ly == 0) return ic + lx;
+    if (ly + 1 == T.th) return ic + T.tw + lx;
+    if (lx == 0) return ic + 2 * T.tw + (ly - 1);
+    return ic + 2 * T.tw + (T.th - 2) + (ly - 1);
+}
+
 // Dynamic shared memory layout (np = blockDim.x node slots):
-//   uint4    sflit[2][4][np]   link flits (input slot d of node i, by parity)
+//   uint4    sflit[2][4][np]   link flits (input slot d of node slot i, by parity)
 //   uint32_t sst[2][4][np]     stamp = the cycle the slot is an input of
+//   uint4    sinj[np]          the flit injected this cycle
 //   uint32_t scnt[NCOUNTERS]
 //   uint32_t shist[3][nb]      (optional)
 template <uint32_t MODE>
@@ -92,7 +122,8 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     extern __shared__ uint4 smem4[];
     const uint32_t np = blockDim.x;
     uint4 *sflit = smem4;
-    uint32_t *sst = reinterpret_cast<uint32_t *>(sflit + 8u * np);
+    uint4 *sinj = sflit + 8u * np;
+    uint32_t *sst = reinterpret_cast<uint32_t *>(sinj + np);
     unsigned int *scnt = sst + 8u * np;
     unsigned int *shist = smem_hist ? scnt + NCOUNTERS : nullptr;
     __shared__ int s_abort;
@@ -110,7 +141,8 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
 
     // ---- node registers (persist for the whole launch)
     NodeCtx c;
-    const uint32_t lx = active ? i % T.tw : 0u, lyy = active ? i / T.tw : 0u;
+    uint32_t lx = 0, lyy = 0;
+    if (active) tile_pos(T, i, lx, lyy);
     c.x = T.x0 + lx;
     c.y = T.y0 + lyy;
     c.n = c.y * S.W + c.x;
@@ -141,12 +173,12 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
         intl = exist & ~ext;
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
-            uint32_t m, mi;
+            uint32_t m = c.l, mi = 0;
             switch (d) {
-            case PN: m = c.l - S.W; mi = i - T.tw; break;
-            case PS: m = c.l + S.W; mi = i + T.tw; break;
-            case PE: m = c.l + 1u; mi = i + 1u; break;
-            default: m = c.l - 1u; mi = i - 1u; break;
+            case PN: m = c.l - S.W; if ((intl >> d) & 1u) mi = tile_slot(T, lx, lyy - 1); break;
+            case PS: m = c.l + S.W; if ((intl >> d) & 1u) mi = tile_slot(T, lx, lyy + 1); break;
+            case PE: m = c.l + 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx + 1, lyy); break;
+            default: m = c.l - 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx - 1, lyy); break;
             }
             if ((ext >> d) & 1u) {
                 inw[d] = (uint32_t)ll_index(S, 0, d, c.l, 0);
@@ -202,58 +234,93 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
             if (MODE == 0u) phase1_ur(S, K, c, t);
             else phase1_lspd(S, K, c, t);
 
-            // Phase 2: latch the internal inputs ...
-            Inputs in;
-            in.present = 0;
+            // Phase 2: which input slots hold a flit this cycle.  All
+            // flits stay in shared memory (slot k<4: sflit, k=4: sinj).
+            uint32_t present = 0;
 #pragma unroll
-            for (uint32_t d = 0; d < 4; ++d) {
-                const uint32_t si = (pb * 4u + d) * np + i;
-                if (((intl >> d) & 1u) && sst[si] == st) {
-                    const uint4 v = sflit[si];
-                    in.f[d] = Flit{v.x, v.y, v.z, v.w};
-                    in.present |= 1u << d;
+            for (uint32_t d = 0; d < 4; ++d)
+                if (((intl >> d) & 1u) && sst[(pb * 4u + d) * np + i] == st) present |= 1u << d;
+            // boundary inputs: spin on the LL stamps, then stage the flit
+            if (ext) {
+#pragma unroll
+                for (uint32_t d = 0; d < 4; ++d) {
+                    if (!((ext >> d) & 1u)) continue;
+                    const unsigned long long *slot = llp + inw[d];
+                    uint32_t spins = 0;
+                    unsigned long long w0 = xa[d], w1 = xb[d], w2 = xc[d], w3 = xd[d];
+                    // complete when word 0 carries this cycle's stamp and, for a
+                    // flit (not EMPTY), so do words 1..3
+                    while ((uint32_t)w0 != st ||
+                           ((uint32_t)(w0 >> 32) != LL_EMPTY &&
+                            ((uint32_t)w1 != st || (uint32_t)w2 != st || (uint32_t)w3 != st))) {
+                        if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
+                        ld_relaxed_x2(slot, w0, w1);
+                        ld_relaxed_x2(slot + 2, w2, w3);
+                    }
+                    const uint32_t x = (uint32_t)(w0 >> 32);
+                    if ((uint32_t)w0 == st && x != LL_EMPTY) {
+                        sflit[(pb * 4u + d) * np + i] =
+                            make_uint4(x, (uint32_t)(w1 >> 32), (uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32));
+                        present |= 1u << d;
+                    }
                 }
             }
-            // ... and the boundary inputs (spin on the stamp)
-#pragma unroll
-            for (uint32_t d = 0; d < 4; ++d) {
-                if (!((ext >> d) & 1u)) continue;
-                const unsigned long long *slot = llp + inw[d];
-                uint32_t spins = 0;
-                unsigned long long w0 = xa[d], w1 = xb[d], w2 = xc[d], w3 = xd[d];
-                // the slot is complete when word 0 carries this cycle's stamp
-                // and, for a flit (not EMPTY), so do words 1..3
-                while ((uint32_t)w0 != st ||
-                       ((uint32_t)(w0 >> 32) != LL_EMPTY &&
-                        ((uint32_t)w1 != st || (uint32_t)w2 != st || (uint32_t)w3 != st))) {
-                    if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
-                    ld_relaxed_x2(slot, w0, w1);
-                    ld_relaxed_x2(slot + 2, w2, w3);
-                }
-                const uint32_t x = (uint32_t)(w0 >> 32);
-                if ((uint32_t)w0 == st && x != LL_EMPTY) {
-                    in.f[d] = Flit{x, (uint32_t)(w1 >> 32), (uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32)};
-                    in.present |= 1u << d;
+            {
+                Flit fi;
+                if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, fi)) {
+                    sinj[i] = make_uint4(fi.x, fi.y, fi.z, fi.w);
+                    present |= 16u;
                 }
             }
-
-            inject(S, c, in, t, acc);
+            auto slot_flit = [&](uint32_t k) -> Flit {
+                const uint4 v = k < 4u ? sflit[(pb * 4u + k) * np + i] : sinj[i];
+                return Flit{v.x, v.y, v.z, v.w};
+            };
+            auto out = [&](uint32_t p, const Flit &f) {
+                const uint32_t slot = p ^ 1u;   // opp(p): N<->S (0,1), E<->W (2,3)
+                if ((ext >> p) & 1u) {
+                    unsigned long long *o = lln + pick4(outw, p);
+                    st_relaxed_x2(o + 2, llw(stn, f.z), llw(stn, f.w));
+                    st_relaxed_x2(o, llw(stn, f.x), llw(stn, f.y));
+                } else {
+                    const uint32_t so = (nb1 * 4u + slot) * np + pick4(outi, p);
+                    sflit[so] = make_uint4(f.x, f.y, f.z, f.w);
+                    sst[so] = stn;
+                }
+            };
             Flit ej;
             bool has_ej = false;
             uint32_t used = 0;
-            if (in.present) {
-                used = route(S, c, in, t, acc, ej, has_ej, [&](uint32_t p, const Flit &f) {
-                    const uint32_t slot = p ^ 1u;   // opp(p): N<->S (0,1), E<->W (2,3)
-                    if ((ext >> p) & 1u) {
-                        unsigned long long *o = lln + pick4(outw, p);
-                        st_relaxed_x2(o + 2, llw(stn, f.z), llw(stn, f.w));
-                        st_relaxed_x2(o, llw(stn, f.x), llw(stn, f.y));
-                    } else {
-                        const uint32_t so = (nb1 * 4u + slot) * np + pick4(outi, p);
-                        sflit[so] = make_uint4(f.x, f.y, f.z, f.w);
-                        sst[so] = stn;
+            if (present) {
+                // fast path over the present slots only: if the first choices
+                // are pairwise distinct, every flit takes its first choice
+                uint32_t seen = 0, fcs = 0;
+                bool coll = false;
+                for (uint32_t m = present; m; m &= m - 1u) {
+                    const uint32_t k = __ffs(m) - 1u;
+                    const uint32_t fc = first_choice(S, c, slot_flit(k), st);
+                    coll |= (seen >> fc) & 1u;
+                    seen |= 1u << fc;
+                    fcs |= fc << (4u * k);
+                }
+                if (!coll) {
+                    for (uint32_t m = present; m; m &= m - 1u) {
+                        const uint32_t k = __ffs(m) - 1u, fc = (fcs >> (4u * k)) & 15u;
+                        const Flit f = slot_flit(k);
+                        if (fc == PX) { ej = f; has_ej = true; continue; }
+                        ++acc.hops;
+                        out(fc, f);
                     }
-                });
+                    used = seen & 15u;
+                } else {
+                    // general case: full ranking + greedy
+                    Inputs in;
+                    in.present = present;
+#pragma unroll
+                    for (uint32_t k = 0; k < 5; ++k)
+                        if ((present >> k) & 1u) in.f[k] = slot_flit(k);
+                    used = route_select(S, c, in, t, acc, ej, has_ej, out);
+                }
             }
             // boundary ports without a flit carry an explicit EMPTY every cycle
             const uint32_t idle_ext = ext & ~used;
@@ -355,7 +422,7 @@ __global__ void k_ll_reset(Dev S, uint64_t t)
 // ------------------------------------------------------------------ host side
 size_t tiled_smem_bytes(const Dev &S, uint32_t np, bool with_hist)
 {
-    return (size_t)np * (8u * 16u + 8u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
+    return (size_t)np * (9u * 16u + 8u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
 }
 
 // Pick TX x TY tiles (<= TILE_MIN_BLOCKS CTAs per SM, <= TILE_BLOCK_MAX nodes
