@@ -90,7 +90,11 @@ typedef struct noc_sim_config {
     int32_t  rank;             /* this process's band, 0..world_size-1            */
     uint32_t engine;           /* NOC_ENGINE_*                                     */
     uint8_t  nccl_id[128];     /* ncclUniqueId from rank 0 (world_size > 1)       */
-    uint32_t reserved[8];      /* must be 0                                        */
+    uint32_t bands;            /* world_size == 1 only: simulate the mesh as this
+                                  many row bands on one GPU ("virtual bands", the
+                                  multi-GPU partition on one device); 0/1 = none.
+                                  Results are identical for every value.         */
+    uint32_t reserved[7];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list
@@ -123,6 +127,16 @@ typedef struct noc_sim noc_sim;
 
 /* ABI version of the loaded library (== NOC_SIM_ABI_VERSION). */
 uint32_t noc_sim_abi_version(void);
+
+/* Row bands (DESIGN 8).  Band g of P covers rows [g*H/P, (g+1)*H/P); it owns
+ * those nodes' links, cores, FIFOs, L2 slices and the directory entries of the
+ * tags homed on them (T mod N in the band).  With world_size = P processes
+ * (one GPU each, torchrun), band = rank; the links crossing a band edge are
+ * written by the sending GPU directly into the receiving GPU's boundary slots
+ * (CUDA IPC over NVLink), NCCL is used for setup and the statistics / hash /
+ * drain reductions.  Fills out[128] with a fresh ncclUniqueId (rank 0 calls
+ * this and broadcasts it).  Errors: NOC_ENCCL. */
+int noc_sim_nccl_unique_id(uint8_t out[128]);
 
 /* Create a simulation at cycle 0 ("initialize" kernel): all links and
  * FIFOs empty, cores IDLE, L2 lines invalid, directory empty, counters 0.

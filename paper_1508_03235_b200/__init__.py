@@ -43,7 +43,8 @@ class noc_sim_config(C.Structure):
         ("sendq_cap", C.c_uint32), ("hist_bins", C.c_uint32), ("seed", C.c_uint64),
         ("script", C.POINTER(noc_sim_event)), ("n_script", C.c_uint64),
         ("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
-        ("engine", C.c_uint32), ("nccl_id", C.c_uint8 * 128), ("reserved", C.c_uint32 * 8),
+        ("engine", C.c_uint32), ("nccl_id", C.c_uint8 * 128), ("bands", C.c_uint32),
+        ("reserved", C.c_uint32 * 7),
     ]
 
 
@@ -89,6 +90,7 @@ def lib():
         L.noc_sim_get_info.argtypes = [P, C.POINTER(noc_sim_info)]
         L.noc_sim_destroy.argtypes = [P]
         L.noc_sim_last_error.restype = C.c_char_p
+        L.noc_sim_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
         if L.noc_sim_abi_version() != 1:
             raise NocSimError(NOC_EINVAL, "ABI version mismatch")
         _lib = L
@@ -102,7 +104,7 @@ def _check(rc):
 
 
 def make_config(cfg: dict, script=None, device: int = 0, engine: int = ENGINE_AUTO,
-                world_size: int = 1, rank: int = 0, nccl_id: bytes = b""):
+                world_size: int = 1, rank: int = 0, nccl_id: bytes = b"", bands: int = 0):
     """Marshal a workloads.py dict (+ script events) into noc_sim_config.
     Returns (config, keepalive)."""
     c = noc_sim_config()
@@ -117,15 +119,15 @@ def make_config(cfg: dict, script=None, device: int = 0, engine: int = ENGINE_AU
         c.script = C.cast(ev, C.POINTER(noc_sim_event))
         c.n_script = len(script)
         keep = ev
-    c.device, c.engine, c.world_size, c.rank = device, engine, world_size, rank
+    c.device, c.engine, c.world_size, c.rank, c.bands = device, engine, world_size, rank, bands
     for i, b in enumerate(nccl_id[:128]):
         c.nccl_id[i] = b
     return c, keep
 
 
 def noc_sim_create(cfg: dict, script=None, device: int = 0, engine: int = ENGINE_AUTO,
-                   world_size: int = 1, rank: int = 0, nccl_id: bytes = b""):
-    c, _keep = make_config(cfg, script, device, engine, world_size, rank, nccl_id)
+                   world_size: int = 1, rank: int = 0, nccl_id: bytes = b"", bands: int = 0):
+    c, _keep = make_config(cfg, script, device, engine, world_size, rank, nccl_id, bands)
     h = C.c_void_p()
     _check(lib().noc_sim_create(C.byref(c), C.byref(h)))
     return h
@@ -170,6 +172,13 @@ def noc_sim_get_info(h) -> dict:
     i = noc_sim_info()
     _check(lib().noc_sim_get_info(h, C.byref(i)))
     return {k: getattr(i, k) for k, _ in noc_sim_info._fields_ if k != "reserved"}
+
+
+def noc_sim_nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for world_size > 1 (rank 0 calls it)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().noc_sim_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def noc_sim_destroy(h):

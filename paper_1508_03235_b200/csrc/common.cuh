@@ -168,6 +168,12 @@ struct Dev {
     // is flit.x or LL_EMPTY; words 1..3 carry flit.y, .z, .w.  Null otherwise.
     uint32_t TX, TY;
     unsigned long long *ll;
+    // row bands (DESIGN 8): the LL arrays of the bands north (0) and south (1)
+    // of this one, and their node counts; a link leaving the band is written
+    // into the receiver band's array (another GPU's memory, mapped by CUDA
+    // IPC, when bands are processes).  Null / 0 at the mesh edge.
+    unsigned long long *ll_nb[2];
+    uint32_t nloc_nb[2];
 };
 
 constexpr uint32_t LL_EMPTY = 0xFFFFFFFFu;   // dst field all ones: never a node (N <= 2^21-1)
@@ -192,8 +198,8 @@ __host__ __device__ __forceinline__ bool slot_external(const Dev &S, uint32_t x,
     if (!S.ll) return false;
     const uint32_t ly = y - S.row0;
     switch (d) {
-    case PN: return y > 0 && tile_of(ly, S.rows, S.TY) != tile_of(ly - 1u, S.rows, S.TY);
-    case PS: return y + 1 < S.H && tile_of(ly, S.rows, S.TY) != tile_of(ly + 1u, S.rows, S.TY);
+    case PN: return y > 0 && (ly == 0 || tile_of(ly, S.rows, S.TY) != tile_of(ly - 1u, S.rows, S.TY));
+    case PS: return y + 1 < S.H && (ly + 1 == S.rows || tile_of(ly, S.rows, S.TY) != tile_of(ly + 1u, S.rows, S.TY));
     case PE: return x + 1 < S.W && tile_of(x, S.W, S.TX) != tile_of(x + 1u, S.W, S.TX);
     default: return x > 0 && tile_of(x, S.W, S.TX) != tile_of(x - 1u, S.W, S.TX);
     }

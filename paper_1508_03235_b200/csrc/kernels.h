@@ -8,10 +8,24 @@ constexpr uint32_t PERSIST_BLOCK = 256;
 constexpr uint32_t TILE_BLOCK_MAX = 512;                  // nodes (= threads) per CTA
 constexpr uint32_t TILE_MIN_BLOCKS = 1;                   // co-resident CTAs per SM
 
-// TILED engine (tile_engine.cu): configure picks the tiling (sets S.TX, S.TY)
-cudaError_t tiled_configure(Dev &S, int device, uint32_t *grid, uint32_t *tpad, uint32_t *smem_hist);
-cudaError_t launch_tiled(const Dev &S, uint64_t t0, uint32_t ncyc, uint32_t grid, uint32_t tpad, uint32_t smem_hist,
+// Row bands handled by one process (virtual bands on one GPU, or the single
+// band of a rank); every band's tiles run in one cooperative launch.
+constexpr uint32_t MAX_BANDS = 8;
+struct DevSet {
+    Dev d[MAX_BANDS];
+    uint32_t nbands;
+    uint32_t tile0[MAX_BANDS + 1];   // first CTA of each band
+};
+
+// TILED engine (tile_engine.cu): tiled_plan picks the tiling of one band
+// (sets S.TX, S.TY) within tiles_budget CTAs; tiled_prepare sets the launch
+// attributes for all bands' tiles in one cooperative launch
+bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np);
+cudaError_t tiled_prepare(uint32_t mode, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
+                          uint32_t *smem_hist);
+cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,
                          uint32_t *activity, cudaStream_t st);
+cudaError_t launch_ll_refresh(const Dev &S, uint64_t t0, cudaStream_t st);
 cudaError_t launch_ll_reset(const Dev &S, uint64_t t, cudaStream_t st);
 
 cudaError_t launch_step(const Dev &S, uint64_t t, uint32_t *activity, cudaStream_t st);

@@ -1,8 +1,11 @@
 // runtime.cu -- host runtime behind include/noc_sim.h: configuration
-// validation, structure-of-arrays allocation in HBM, engine selection and
-// launch control, drain, statistics and the canonical state hash.
+// validation, structure-of-arrays allocation in HBM (per row band), engine
+// selection and launch control, drain, statistics and the canonical state
+// hash, and the multi-GPU row-band plumbing (CUDA IPC + NCCL).
 #include "../../include/noc_sim.h"
 #include "kernels.h"
+
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -30,23 +33,50 @@ extern "C" uint32_t noc_sim_abi_version(void) { return NOC_SIM_ABI_VERSION; }
             return fail(NOC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));           \
     } while (0)
 
+#define NC(call)                                                                                  \
+    do {                                                                                          \
+        ncclResult_t r_ = (call);                                                                 \
+        if (r_ != ncclSuccess)                                                                    \
+            return fail(NOC_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));           \
+    } while (0)
+
+extern "C" int noc_sim_nccl_unique_id(uint8_t out[128])
+{
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    memcpy(out, &id, 128);
+    return NOC_OK;
+}
+
 struct noc_sim {
     noc_sim_config cfg;
-    Dev D;
+    int nb = 1;                 // bands simulated by this process
+    int P = 1;                  // bands in the whole mesh
+    int g0 = 0;                 // global index of the first local band
+    Dev D[MAX_BANDS];
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    uint64_t t = 0;               // next cycle to simulate
+    uint64_t t = 0;             // next cycle to simulate
     uint32_t engine = NOC_ENGINE_STEP;
     // persistent engine
     uint32_t *progress = nullptr;
     uint32_t pbase = 0;
     uint32_t p_grid = 0, p_npc = 0, p_smem_hist = 0;
     // tiled engine
-    uint32_t t_grid = 0, t_tpad = 0, t_smem_hist = 0;
-    // scratch
+    DevSet set;
+    uint32_t t_tpad = 0, t_smem_hist = 0;
+    // shared by the bands of this process
+    unsigned long long *cnt = nullptr, *hist = nullptr;
+    uint32_t *err = nullptr;
     uint32_t *d_scratch = nullptr;          // [DRAIN_CHUNK + 2]
     unsigned long long *d_hash = nullptr;
+    unsigned long long *d_red = nullptr;    // reduction buffer (NCCL)
+    // multi-GPU
+    int world = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    std::vector<void *> ipc_opened;
     std::vector<void *> allocs;
     uint64_t bytes = 0, loc_bytes = 0;
     uint64_t launches = 0;
@@ -94,9 +124,12 @@ static int validate(const noc_sim_config *c)
     }
     if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size)
         return fail(NOC_EINVAL, "bad world_size/rank");
-    if (c->world_size > 1) return fail(NOC_EINVAL, "world_size > 1 is not built into this library version");
+    if (c->world_size > (int)MAX_BANDS || c->world_size > (int)c->mesh_h)
+        return fail(NOC_EINVAL, "world_size must be <= 8 and <= mesh_h");
+    if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
+    if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED) return fail(NOC_EINVAL, "unknown engine");
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 7; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->n_script && !c->script) return fail(NOC_EINVAL, "n_script > 0 with a null script");
     for (uint64_t i = 0; i < c->n_script; ++i) {
@@ -117,12 +150,145 @@ extern "C" void noc_sim_destroy(noc_sim *s)
     cudaGetDevice(&cur);
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
+    for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (s->comm) ncclCommDestroy(s->comm);
     for (void *p : s->allocs) cudaFree(p);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->stream) cudaStreamDestroy(s->stream);
     cudaSetDevice(cur);
     delete s;
+}
+
+// rows of band g of P
+static void band_rows(uint32_t H, int P, int g, uint32_t *row0, uint32_t *rows)
+{
+    uint32_t a = (uint32_t)((uint64_t)g * H / P), b = (uint32_t)((uint64_t)(g + 1) * H / P);
+    *row0 = a;
+    *rows = b - a;
+}
+
+// allocate and initialise the state of one band (DESIGN 6.1)
+static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
+{
+    int rc;
+    memset(&D, 0, sizeof D);
+    D.W = cfg->mesh_w;
+    D.H = cfg->mesh_h;
+    D.N = D.W * D.H;
+    band_rows(D.H, s->P, g, &D.row0, &D.rows);
+    D.n0 = D.row0 * D.W;
+    D.nloc = D.rows * D.W;
+    D.mode = cfg->mode;
+    D.prio = cfg->prio;
+    D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
+    D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
+    D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
+    D.priv = cfg->priv_tags;
+    D.thr_inj = cfg->thr_inj;
+    D.thr_priv = cfg->thr_priv;
+    D.l2_hit_lat = cfg->l2_hit_lat;
+    D.mem_lat = cfg->mem_lat;
+    D.nfl_ra = cfg->nfl_ra;
+    D.qcap = cfg->sendq_cap;
+    D.nb = cfg->hist_bins;
+    D.seed_lo = (uint32_t)cfg->seed;
+    D.seed_hi = (uint32_t)(cfg->seed >> 32);
+    D.gen = 1;
+    D.wmagic = (uint32_t)(((1ull << 32) + D.W - 1) / D.W);
+    D.cnt = s->cnt;
+    D.hist = s->hist;
+    D.err = s->err;
+    const size_t n = D.nloc;
+    for (int b = 0; b < 2; ++b) {
+        if ((rc = dalloc(s, &D.flit[b], 4 * n))) return rc;
+        if ((rc = dalloc(s, &D.flag[b], n))) return rc;
+    }
+    if ((rc = dalloc(s, &D.fifo_ctl, n))) return rc;
+    if ((rc = dalloc(s, &D.fifo_pkt, n * D.qcap))) return rc;
+    if (cfg->mode == NOC_MODE_LSPD) {
+        if ((rc = dalloc(s, &D.core_hot, n))) return rc;
+        if ((rc = dalloc(s, &D.core_cold, n))) return rc;
+        if ((rc = dalloc(s, &D.l2, n * D.sets * D.ways))) return rc;
+        uint64_t b0 = s->bytes;
+        if ((rc = dalloc(s, &D.loc, (size_t)D.tpn * n))) return rc;
+        s->loc_bytes += s->bytes - b0;
+    }
+    // script events of this band's nodes, per node ordered by (cycle, input order)
+    std::vector<uint32_t> off(n + 1, 0);
+    std::vector<uint4> ev;
+    if (cfg->n_script) {
+        std::vector<uint64_t> idx;
+        for (uint64_t i = 0; i < cfg->n_script; ++i)
+            if (cfg->script[i].node >= D.n0 && cfg->script[i].node < D.n0 + D.nloc) idx.push_back(i);
+        std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
+            const noc_sim_event &x = cfg->script[a], &y = cfg->script[b];
+            if (x.node != y.node) return x.node < y.node;
+            return x.cycle < y.cycle;
+        });
+        ev.resize(idx.size());
+        for (size_t i = 0; i < idx.size(); ++i) {
+            const noc_sim_event &x = cfg->script[idx[i]];
+            ev[i] = make_uint4((uint32_t)x.cycle, (uint32_t)(x.cycle >> 32), x.value, 0u);
+            off[x.node - D.n0 + 1] += 1;
+        }
+        for (size_t i = 0; i < n; ++i) off[i + 1] += off[i];
+        D.has_script = 1;
+    }
+    uint4 *dev_ev = nullptr;
+    uint32_t *dev_off = nullptr;
+    if ((rc = dalloc(s, &dev_ev, ev.size()))) return rc;
+    if ((rc = dalloc(s, &dev_off, n + 1))) return rc;
+    if ((rc = dalloc(s, &D.script_pos, n))) return rc;
+    if (!ev.empty()) CU(cudaMemcpy(dev_ev, ev.data(), ev.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dev_off, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    D.script = dev_ev;
+    D.script_off = dev_off;
+    return NOC_OK;
+}
+
+// stream-ordered barrier / reductions across ranks (no-ops when world == 1)
+static int allreduce_u64(noc_sim *s, unsigned long long *buf, size_t count)
+{
+    if (s->world == 1) return NOC_OK;
+    NC(ncclAllReduce(buf, buf, count, ncclUint64, ncclSum, s->comm, s->stream));
+    return NOC_OK;
+}
+static int allreduce_u32(noc_sim *s, uint32_t *buf, size_t count)
+{
+    if (s->world == 1) return NOC_OK;
+    NC(ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, s->comm, s->stream));
+    return NOC_OK;
+}
+
+// multi-GPU: map the neighbour bands' boundary slots (CUDA IPC over NVLink)
+static int link_ranks(noc_sim *s)
+{
+    Dev &D = s->D[0];
+    cudaIpcMemHandle_t mine;
+    CU(cudaIpcGetMemHandle(&mine, D.ll));
+    uint8_t *dev_h = nullptr;
+    int rc;
+    if ((rc = dalloc(s, &dev_h, (size_t)64 * s->world))) return rc;
+    CU(cudaMemcpy(dev_h + 64 * s->rank, &mine, 64, cudaMemcpyHostToDevice));
+    NC(ncclAllGather(dev_h + 64 * s->rank, dev_h, 64, ncclUint8, s->comm, s->stream));
+    std::vector<uint8_t> all((size_t)64 * s->world);
+    CU(cudaMemcpyAsync(all.data(), dev_h, all.size(), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    for (int side = 0; side < 2; ++side) {
+        const int r = side == 0 ? s->rank - 1 : s->rank + 1;
+        if (r < 0 || r >= s->world) continue;
+        cudaIpcMemHandle_t h;
+        memcpy(&h, all.data() + 64 * r, 64);
+        void *p = nullptr;
+        CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        s->ipc_opened.push_back(p);
+        uint32_t row0, rows;
+        band_rows(D.H, s->P, r, &row0, &rows);
+        D.ll_nb[side] = (unsigned long long *)p;
+        D.nloc_nb[side] = rows * D.W;
+    }
+    return NOC_OK;
 }
 
 extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
@@ -141,126 +307,90 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     s->cfg = *cfg;
     s->cfg.script = nullptr;
     s->device = cfg->device;
+    s->world = cfg->world_size;
+    s->rank = cfg->rank;
+    if (s->world > 1) { s->nb = 1; s->P = s->world; s->g0 = s->rank; }
+    else { s->nb = cfg->bands > 1 ? (int)cfg->bands : 1; s->P = s->nb; s->g0 = 0; }
     auto bail = [&](int code) { noc_sim_destroy(s); return code; };
     if (cudaSetDevice(s->device) != cudaSuccess) return bail(fail(NOC_ECUDA, "cudaSetDevice failed"));
     cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, s->device);
     if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess)
         return bail(fail(NOC_ECUDA, "stream/event creation failed"));
+    if (s->world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_id, 128);
+        ncclResult_t r = ncclCommInitRank(&s->comm, s->world, id, s->rank);
+        if (r != ncclSuccess) return bail(fail(NOC_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+    }
 
-    Dev &D = s->D;
-    memset(&D, 0, sizeof D);
-    D.W = cfg->mesh_w;
-    D.H = cfg->mesh_h;
-    D.N = D.W * D.H;
-    D.row0 = 0;
-    D.rows = D.H;
-    D.n0 = 0;
-    D.nloc = D.N;
-    D.mode = cfg->mode;
-    D.prio = cfg->prio;
-    D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
-    D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
-    D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
-    D.priv = cfg->priv_tags;
-    D.thr_inj = cfg->thr_inj;
-    D.thr_priv = cfg->thr_priv;
-    D.l2_hit_lat = cfg->l2_hit_lat;
-    D.mem_lat = cfg->mem_lat;
-    D.nfl_ra = cfg->nfl_ra;
-    D.qcap = cfg->sendq_cap;
-    D.nb = cfg->hist_bins;
-    D.seed_lo = (uint32_t)cfg->seed;
-    D.seed_hi = (uint32_t)(cfg->seed >> 32);
-    D.gen = 1;
-    D.wmagic = (uint32_t)(((1ull << 32) + D.W - 1) / D.W);
-    const size_t n = D.nloc;
-
-    for (int b = 0; b < 2; ++b) {
-        if ((rc = dalloc(s, &D.flit[b], 4 * n))) return bail(rc);
-        if ((rc = dalloc(s, &D.flag[b], n))) return bail(rc);
-    }
-    if ((rc = dalloc(s, &D.fifo_ctl, n))) return bail(rc);
-    if ((rc = dalloc(s, &D.fifo_pkt, n * D.qcap))) return bail(rc);
-    if ((rc = dalloc(s, &D.cnt, NCOUNTERS))) return bail(rc);
-    if ((rc = dalloc(s, &D.hist, 3 * (size_t)D.nb))) return bail(rc);
-    if ((rc = dalloc(s, &D.err, 1))) return bail(rc);
-    if (cfg->mode == NOC_MODE_LSPD) {
-        if ((rc = dalloc(s, &D.core_hot, n))) return bail(rc);
-        if ((rc = dalloc(s, &D.core_cold, n))) return bail(rc);
-        if ((rc = dalloc(s, &D.l2, n * D.sets * D.ways))) return bail(rc);
-        uint64_t b0 = s->bytes;
-        if ((rc = dalloc(s, &D.loc, (size_t)D.tpn * n))) return bail(rc);
-        s->loc_bytes = s->bytes - b0;
-    }
-    // script: per node, ordered by (cycle, input order)
-    {
-        std::vector<uint32_t> off(n + 1, 0);
-        std::vector<uint4> ev;
-        if (cfg->n_script) {
-            std::vector<uint64_t> idx(cfg->n_script);
-            for (uint64_t i = 0; i < cfg->n_script; ++i) idx[i] = i;
-            std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
-                const noc_sim_event &x = cfg->script[a], &y = cfg->script[b];
-                if (x.node != y.node) return x.node < y.node;
-                return x.cycle < y.cycle;
-            });
-            ev.resize(cfg->n_script);
-            for (uint64_t i = 0; i < cfg->n_script; ++i) {
-                const noc_sim_event &x = cfg->script[idx[i]];
-                ev[i] = make_uint4((uint32_t)x.cycle, (uint32_t)(x.cycle >> 32), x.value, 0u);
-                off[x.node + 1] += 1;
-            }
-            for (size_t i = 0; i < n; ++i) off[i + 1] += off[i];
-            D.has_script = 1;
-        }
-        uint4 *dev_ev = nullptr;
-        uint32_t *dev_off = nullptr;
-        if ((rc = dalloc(s, &dev_ev, ev.size()))) return bail(rc);
-        if ((rc = dalloc(s, &dev_off, n + 1))) return bail(rc);
-        if ((rc = dalloc(s, &D.script_pos, n))) return bail(rc);
-        if (!ev.empty() && cudaMemcpy(dev_ev, ev.data(), ev.size() * sizeof(uint4), cudaMemcpyHostToDevice) != cudaSuccess)
-            return bail(fail(NOC_ECUDA, "script upload failed"));
-        if (cudaMemcpy(dev_off, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess)
-            return bail(fail(NOC_ECUDA, "script upload failed"));
-        D.script = dev_ev;
-        D.script_off = dev_off;
-    }
+    if ((rc = dalloc(s, &s->cnt, NCOUNTERS))) return bail(rc);
+    if ((rc = dalloc(s, &s->hist, 3 * (size_t)cfg->hist_bins))) return bail(rc);
+    if ((rc = dalloc(s, &s->err, 1))) return bail(rc);
     if ((rc = dalloc(s, &s->d_scratch, DRAIN_CHUNK + 2))) return bail(rc);
     if ((rc = dalloc(s, &s->d_hash, 1))) return bail(rc);
+    if ((rc = dalloc(s, &s->d_red, NCOUNTERS + 3 * (size_t)cfg->hist_bins + 2))) return bail(rc);
+    for (int k = 0; k < s->nb; ++k)
+        if ((rc = make_band(s, cfg, s->g0 + k, s->D[k]))) return bail(rc);
 
-    // engine: TILED when every tile fits one CTA of <= TILE_MAX_THREADS
-    // threads on its own SM, else PERSIST (DESIGN 6)
+    // engine: TILED when every band's tiles fit one CTA of <= TILE_BLOCK_MAX
+    // threads per SM, else PERSIST (DESIGN 6.2); bands require TILED
     s->engine = cfg->engine;
+    if (s->P > 1 && s->engine != NOC_ENGINE_AUTO && s->engine != NOC_ENGINE_TILED)
+        return bail(fail(NOC_EINVAL, "row bands need the TILED engine"));
     if (s->engine == NOC_ENGINE_AUTO || s->engine == NOC_ENGINE_TILED) {
-        Dev trial = D;
-        uint32_t g = 0, tp = 0, sh = 0;
-        cudaError_t ce = tiled_configure(trial, s->device, &g, &tp, &sh);
+        bool ok = true;
+        uint32_t np = 32, total = 0;
+        const uint32_t budget = std::max<uint32_t>(1u, (uint32_t)s->sm_count / (uint32_t)s->nb);
+        s->set.nbands = (uint32_t)s->nb;
+        s->set.tile0[0] = 0;
+        for (int k = 0; k < s->nb && ok; ++k) {
+            uint32_t tiles = 0, npk = 0;
+            ok = tiled_plan(s->D[k], budget, &tiles, &npk);
+            np = std::max(np, npk);
+            total += tiles;
+            s->set.tile0[k + 1] = total;
+        }
+        cudaError_t ce = ok ? tiled_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
+                            : cudaErrorInvalidConfiguration;
         if (ce == cudaSuccess) {
             s->engine = NOC_ENGINE_TILED;
-            D.TX = trial.TX;
-            D.TY = trial.TY;
-            s->t_grid = g;
-            s->t_tpad = tp;
-            s->t_smem_hist = sh;
-        } else if (s->engine == NOC_ENGINE_TILED) {
-            cudaGetLastError();
-            return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") + cudaGetErrorString(ce)));
+            s->t_tpad = np;
         } else {
             cudaGetLastError();
+            if (s->engine == NOC_ENGINE_TILED || s->P > 1)
+                return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") +
+                                                 cudaGetErrorString(ce)));
             s->engine = NOC_ENGINE_PERSIST;
         }
     }
     if (s->engine == NOC_ENGINE_TILED) {
-        if ((rc = dalloc(s, &D.ll, (size_t)32u * n))) return bail(rc);
-        if (launch_ll_reset(D, 0, s->stream) != cudaSuccess) return bail(fail(NOC_ECUDA, "ll reset failed"));
+        for (int k = 0; k < s->nb; ++k)
+            if ((rc = dalloc(s, &s->D[k].ll, (size_t)32u * s->D[k].nloc))) return bail(rc);
+        // neighbour bands' boundary slots
+        if (s->world > 1) {
+            if ((rc = link_ranks(s))) return bail(rc);
+        } else {
+            for (int k = 0; k < s->nb; ++k) {
+                if (k > 0) { s->D[k].ll_nb[0] = s->D[k - 1].ll; s->D[k].nloc_nb[0] = s->D[k - 1].nloc; }
+                if (k + 1 < s->nb) { s->D[k].ll_nb[1] = s->D[k + 1].ll; s->D[k].nloc_nb[1] = s->D[k + 1].nloc; }
+            }
+        }
+        for (int k = 0; k < s->nb; ++k) {
+            if (launch_ll_reset(s->D[k], 0, s->stream) != cudaSuccess) return bail(fail(NOC_ECUDA, "ll reset failed"));
+            s->set.d[k] = s->D[k];
+        }
     }
     if (s->engine == NOC_ENGINE_PERSIST) {
-        cudaError_t ce = persist_configure(D, s->device, &s->p_grid, &s->p_npc, &s->p_smem_hist);
+        cudaError_t ce = persist_configure(s->D[0], s->device, &s->p_grid, &s->p_npc, &s->p_smem_hist);
         if (ce != cudaSuccess) return bail(fail(NOC_ECUDA, std::string("persist_configure: ") + cudaGetErrorString(ce)));
         if ((rc = dalloc(s, &s->progress, s->p_grid))) return bail(rc);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(NOC_ECUDA, "init sync failed"));
+    if (s->world > 1) {   // every rank has mapped its neighbours before anyone runs
+        if ((rc = allreduce_u32(s, s->d_scratch, 1))) return bail(rc);
+        if (cudaStreamSynchronize(s->stream) != cudaSuccess) return bail(fail(NOC_ECUDA, "init barrier failed"));
+    }
     *out = s;
     return NOC_OK;
 }
@@ -268,15 +398,23 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
 static int check_err(noc_sim *s)
 {
     uint32_t err = 0;
-    CU(cudaMemcpyAsync(&err, s->D.err, 4, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(&err, s->err, 4, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     if (err) {
         s->poisoned = 1;
-        if (err & 0x80000000u) return fail(NOC_ECUDA, "persistent kernel: neighbour wait timed out");
-        if (err & (ERR_AGE | ERR_PEND)) return fail(NOC_EOVERFLOW, "field width exceeded (flit age > 65535 or pend > 1023)");
+        if (err & 0x80000000u) return fail(NOC_ECUDA, "boundary / neighbour wait timed out");
+        if (err & (ERR_AGE | ERR_PEND)) return fail(NOC_EOVERFLOW, "field width exceeded (flit age, lifetime or pend)");
         return fail(NOC_ECUDA, "model assertion failed on device (protocol / EV holder)");
     }
     return NOC_OK;
+}
+
+static void set_gen(noc_sim *s, uint32_t gen)
+{
+    for (int k = 0; k < s->nb; ++k) {
+        s->D[k].gen = gen;
+        s->set.d[k].gen = gen;
+    }
 }
 
 // Advance n cycles with the handle's engine; activity (device, may be null)
@@ -288,9 +426,14 @@ static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
-            e = launch_tiled(s->D, s->t + done, k, s->t_grid, s->t_tpad, s->t_smem_hist,
-                             activity ? activity + done : nullptr, s->stream);
+            for (int b = 0; b < s->nb; ++b) CU(launch_ll_refresh(s->D[b], s->t + done, s->stream));
+            e = launch_tiled(s->set, s->t + done, k, s->t_tpad, s->t_smem_hist, activity ? activity + done : nullptr,
+                             s->stream);
             if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(e));
+            // ranks: the next refresh may only run once the neighbours stopped
+            // writing into this band's boundary slots
+            int rc = allreduce_u32(s, s->d_scratch + DRAIN_CHUNK, 1);
+            if (rc) return rc;
             done += k;
             s->launches += 1;
         }
@@ -298,7 +441,7 @@ static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
-            e = launch_persist(s->D, s->t + done, k, s->progress, s->pbase, s->p_grid, s->p_npc, s->p_smem_hist,
+            e = launch_persist(s->D[0], s->t + done, k, s->progress, s->pbase, s->p_grid, s->p_npc, s->p_smem_hist,
                                activity ? activity + done : nullptr, s->stream);
             if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
             s->pbase += k;
@@ -307,7 +450,7 @@ static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
         }
     } else {
         for (uint64_t i = 0; i < n; ++i) {
-            e = launch_step(s->D, s->t + i, activity ? activity + i : nullptr, s->stream);
+            e = launch_step(s->D[0], s->t + i, activity ? activity + i : nullptr, s->stream);
             if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("step launch: ") + cudaGetErrorString(e));
             s->launches += 1;
         }
@@ -349,11 +492,12 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
     if (s->poisoned) return fail(NOC_ESTATE, "handle poisoned by an earlier error");
     CU(cudaSetDevice(s->device));
     uint64_t t0 = s->t, k = 0;
-    int q = 0;
-    s->D.gen = 0;
+    int q = 0, rc;
+    set_gen(s, 0);
     // quiescent already?
     CU(cudaMemsetAsync(s->d_scratch, 0, 4, s->stream));
-    CU(launch_busy_count(s->D, s->t, s->d_scratch, s->stream));
+    for (int b = 0; b < s->nb; ++b) CU(launch_busy_count(s->D[b], s->t, s->d_scratch, s->stream));
+    if ((rc = allreduce_u32(s, s->d_scratch, 1))) return rc;
     uint32_t busy = 0;
     CU(cudaMemcpyAsync(&busy, s->d_scratch, 4, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
@@ -362,8 +506,9 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
     while (!q && k < max_cycles) {
         uint32_t chunk = (uint32_t)std::min<uint64_t>(DRAIN_CHUNK, max_cycles - k);
         CU(cudaMemsetAsync(s->d_scratch, 0, sizeof(uint32_t) * chunk, s->stream));
-        int rc = advance(s, chunk, s->d_scratch);
-        if (rc) { s->D.gen = 1; return rc; }
+        rc = advance(s, chunk, s->d_scratch);
+        if (rc) { set_gen(s, 1); return rc; }
+        if ((rc = allreduce_u32(s, s->d_scratch, chunk))) return rc;
         CU(cudaMemcpyAsync(act.data(), s->d_scratch, sizeof(uint32_t) * chunk, cudaMemcpyDeviceToHost, s->stream));
         CU(cudaStreamSynchronize(s->stream));
         uint32_t i = 0;
@@ -376,12 +521,14 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
             s->t = t0 + k;
             // boundary slots were stamped up to the end of the chunk: re-stamp
             // them EMPTY for the rewound cycle (nothing is in flight)
-            if (s->engine == NOC_ENGINE_TILED) CU(launch_ll_reset(s->D, s->t, s->stream));
+            if (s->engine == NOC_ENGINE_TILED)
+                for (int b = 0; b < s->nb; ++b) CU(launch_ll_reset(s->D[b], s->t, s->stream));
+            if ((rc = allreduce_u32(s, s->d_scratch + DRAIN_CHUNK, 1))) return rc;
         } else {
             k += chunk;
         }
     }
-    s->D.gen = 1;
+    set_gen(s, 1);
     if (used) *used = k;
     if (drained) *drained = q;
     return check_err(s);
@@ -389,25 +536,44 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
 
 static const int NC_NAMED = 23;
 
+// counters and histograms summed over ranks, on the host
+static int gather_stats(noc_sim *s, std::vector<unsigned long long> &c, std::vector<unsigned long long> &h)
+{
+    const size_t nh = 3 * (size_t)s->cfg.hist_bins;
+    c.resize(NCOUNTERS);
+    h.resize(nh);
+    if (s->world > 1) {
+        CU(cudaMemcpyAsync(s->d_red, s->cnt, NCOUNTERS * 8, cudaMemcpyDeviceToDevice, s->stream));
+        CU(cudaMemcpyAsync(s->d_red + NCOUNTERS, s->hist, nh * 8, cudaMemcpyDeviceToDevice, s->stream));
+        int rc = allreduce_u64(s, s->d_red, NCOUNTERS + nh);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(c.data(), s->d_red, NCOUNTERS * 8, cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaMemcpyAsync(h.data(), s->d_red + NCOUNTERS, nh * 8, cudaMemcpyDeviceToHost, s->stream));
+    } else {
+        CU(cudaMemcpyAsync(c.data(), s->cnt, NCOUNTERS * 8, cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaMemcpyAsync(h.data(), s->hist, nh * 8, cudaMemcpyDeviceToHost, s->stream));
+    }
+    CU(cudaStreamSynchronize(s->stream));
+    return NOC_OK;
+}
+
 extern "C" int noc_sim_stats(noc_sim *s, noc_sim_counters *out, uint64_t *hl, uint64_t *hd, uint64_t *ha, uint32_t nbins)
 {
     if (!s) return fail(NOC_EINVAL, "null handle");
-    if ((hl || hd || ha) && nbins != s->D.nb) return fail(NOC_EINVAL, "nbins != hist_bins");
+    if ((hl || hd || ha) && nbins != s->cfg.hist_bins) return fail(NOC_EINVAL, "nbins != hist_bins");
     CU(cudaSetDevice(s->device));
+    std::vector<unsigned long long> c, h;
+    int rc = gather_stats(s, c, h);
+    if (rc) return rc;
     if (out) {
-        unsigned long long c[NCOUNTERS];
-        CU(cudaMemcpyAsync(c, s->D.cnt, sizeof c, cudaMemcpyDeviceToHost, s->stream));
-        CU(cudaStreamSynchronize(s->stream));
         int64_t *dst = &out->generated;
         out->cycle = (int64_t)s->t;
         for (int i = 0; i < NC_NAMED; ++i) dst[i] = (int64_t)c[i];
         for (int k = 0; k < 8; ++k) out->drops[k] = (int64_t)c[C_DROPS + k];
     }
     uint64_t *hs[3] = {hl, hd, ha};
-    for (int h = 0; h < 3; ++h)
-        if (hs[h]) CU(cudaMemcpyAsync(hs[h], s->D.hist + (size_t)h * s->D.nb, sizeof(uint64_t) * s->D.nb,
-                                      cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
+    for (int k = 0; k < 3; ++k)
+        if (hs[k]) memcpy(hs[k], h.data() + (size_t)k * s->cfg.hist_bins, sizeof(uint64_t) * s->cfg.hist_bins);
     return NOC_OK;
 }
 
@@ -416,20 +582,20 @@ extern "C" int noc_sim_state_hash(noc_sim *s, uint64_t *out)
     if (!s || !out) return fail(NOC_EINVAL, "null argument");
     CU(cudaSetDevice(s->device));
     CU(cudaMemsetAsync(s->d_hash, 0, 8, s->stream));
-    CU(launch_hash(s->D, s->t, s->d_hash, s->stream));
+    for (int b = 0; b < s->nb; ++b) CU(launch_hash(s->D[b], s->t, s->d_hash, s->stream));
+    int rc = allreduce_u64(s, s->d_hash, 1);
+    if (rc) return rc;
     unsigned long long H = 0;
     CU(cudaMemcpyAsync(&H, s->d_hash, 8, cudaMemcpyDeviceToHost, s->stream));
-    unsigned long long c[NCOUNTERS];
-    CU(cudaMemcpyAsync(c, s->D.cnt, sizeof c, cudaMemcpyDeviceToHost, s->stream));
-    std::vector<unsigned long long> hist(3 * (size_t)s->D.nb);
-    CU(cudaMemcpyAsync(hist.data(), s->D.hist, hist.size() * 8, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
+    std::vector<unsigned long long> c, hist;
+    if ((rc = gather_stats(s, c, hist))) return rc;
     uint64_t h = H;
+    const uint32_t nb = s->cfg.hist_bins;
     for (uint32_t i = 0; i < NCOUNTERS; ++i) h += hterm(D_CNT, i, TupleHash(1).add(c[i]).h);
     for (uint32_t k = 0; k < 3; ++k)
-        for (uint32_t b = 0; b < s->D.nb; ++b)
-            if (hist[(size_t)k * s->D.nb + b])
-                h += hterm(D_HIST, ((uint64_t)k << 32) + b, TupleHash(1).add(hist[(size_t)k * s->D.nb + b]).h);
+        for (uint32_t b = 0; b < nb; ++b)
+            if (hist[(size_t)k * nb + b])
+                h += hterm(D_HIST, ((uint64_t)k << 32) + b, TupleHash(1).add(hist[(size_t)k * nb + b]).h);
     h += hterm(D_CYCLE, 0, TupleHash(1).add(s->t).h);
     *out = h;
     return NOC_OK;
@@ -441,24 +607,27 @@ extern "C" int noc_sim_get_info(noc_sim *s, noc_sim_info *o)
     memset(o, 0, sizeof *o);
     o->engine = s->engine;
     if (s->engine == NOC_ENGINE_TILED) {
-        o->grid = s->t_grid;
+        o->grid = s->set.tile0[s->set.nbands];
         o->block = s->t_tpad;
-        o->reserved[0] = (int32_t)s->D.TX;
-        o->reserved[1] = (int32_t)s->D.TY;
+        o->reserved[0] = (int32_t)s->D[0].TX;
+        o->reserved[1] = (int32_t)s->D[0].TY;
     } else if (s->engine == NOC_ENGINE_PERSIST) {
         o->grid = s->p_grid;
         o->block = PERSIST_BLOCK;
     } else {
-        o->grid = (s->D.nloc + 255u) / 256u;
+        o->grid = (s->D[0].nloc + 255u) / 256u;
         o->block = 256;
     }
-    o->nodes_local = s->D.nloc;
-    o->row0 = s->D.row0;
-    o->rows = s->D.rows;
+    uint32_t nl = 0;
+    for (int k = 0; k < s->nb; ++k) nl += s->D[k].nloc;
+    o->nodes_local = nl;
+    o->row0 = s->D[0].row0;
+    o->rows = nl / s->D[0].W;
     o->device_bytes = s->bytes;
     o->loc_bytes = s->loc_bytes;
     o->kernel_launches = s->launches;
     o->cycles_run = s->t;
     o->sm_count = s->sm_count;
+    o->reserved[2] = s->P;
     return NOC_OK;
 }

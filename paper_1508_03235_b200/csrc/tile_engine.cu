@@ -115,10 +115,67 @@ __device__ __forceinline__ uint32_t tile_slot(const TileShape &T, uint32_t lx, u
 //   uint4    sinj[np]          the flit injected this cycle
 //   uint32_t scnt[NCOUNTERS]
 //   uint32_t shist[3][nb]      (optional)
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void ld_relaxed_sys_x2(const unsigned long long *p, unsigned long long &a,
+                                                  unsigned long long &b)
+{
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys_x2(unsigned long long *p, unsigned long long a, unsigned long long b)
+{
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// LL accesses: links inside the band use gpu scope, links across a band edge
+// (possibly another GPU) system scope
+__device__ __forceinline__ void ll_load2(bool sys, const unsigned long long *p, unsigned long long &a,
+                                         unsigned long long &b)
+{
+    if (sys) ld_relaxed_sys_x2(p, a, b);
+    else ld_relaxed_x2(p, a, b);
+}
+__device__ __forceinline__ void ll_store2(bool sys, unsigned long long *p, unsigned long long a, unsigned long long b)
+{
+    if (sys) st_relaxed_sys_x2(p, a, b);
+    else st_relaxed_x2(p, a, b);
+}
+__device__ __forceinline__ void ll_store1(bool sys, unsigned long long *p, unsigned long long a)
+{
+    if (sys) st_relaxed_sys_u64(p, a);
+    else st_relaxed_u64(p, a);
+}
+
+// Base of the LL array (parity nb) that output port p writes into: this band's
+// own array, or the north / south neighbour band's across a band edge.
+__device__ __forceinline__ unsigned long long *ll_out(const Dev &S, bool band_edge, uint32_t p, uint32_t nb,
+                                                     uint32_t pstride)
+{
+    if (!band_edge) return S.ll + (size_t)nb * pstride;
+    const uint32_t side = p == PN ? 0u : 1u;
+    return S.ll_nb[side] + (size_t)nb * 16u * S.nloc_nb[side];
+}
+
 template <uint32_t MODE>
 __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
-k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
+k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
 {
+    // this CTA's band and tile
+    uint32_t band = 0;
+    while (band + 1 < P.nbands && blockIdx.x >= P.tile0[band + 1]) ++band;
+    const Dev &S = P.d[band];
+    const uint32_t tile = blockIdx.x - P.tile0[band];
     extern __shared__ uint4 smem4[];
     const uint32_t np = blockDim.x;
     uint4 *sflit = smem4;
@@ -130,7 +187,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     __shared__ uint32_t s_busy[2];
 
     const uint32_t i = threadIdx.x;
-    const TileShape T = tile_shape(S, blockIdx.x);
+    const TileShape T = tile_shape(S, tile);
     const bool active = i < T.tn;
 
     {
@@ -157,6 +214,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
     c.cold = make_uint4(0, 0, 0, 0);
     uint32_t ext = 0;      // bit d: port d crosses the tile boundary
     uint32_t intl = 0;     // bit d: port d exists inside the tile
+    uint32_t bedge = 0;    // bit d: port d crosses the band edge (N: 0, S: 1)
     uint32_t inw[4] = {0, 0, 0, 0}, outw[4] = {0, 0, 0, 0}, outi[4] = {0, 0, 0, 0};
     const uint32_t b0 = (uint32_t)t0 & 1u;
     if (active) {
@@ -171,6 +229,7 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
         ext = ((lyy == 0 ? 1u : 0u) | (lyy + 1 == T.th ? 2u : 0u) | (lx + 1 == T.tw ? 4u : 0u) |
                (lx == 0 ? 8u : 0u)) & exist;
         intl = exist & ~ext;
+        bedge = ((c.y == S.row0 && c.y > 0) ? 1u : 0u) | ((c.y + 1 == S.row0 + S.rows && c.y + 1 < S.H) ? 2u : 0u);
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
             uint32_t m = c.l, mi = 0;
@@ -182,7 +241,14 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
             }
             if ((ext >> d) & 1u) {
                 inw[d] = (uint32_t)ll_index(S, 0, d, c.l, 0);
-                outw[d] = (uint32_t)ll_index(S, 0, d ^ 1u, m, 0);
+                if ((bedge >> d) & 1u) {
+                    // the receiver is in the neighbour band: its local index there
+                    const uint32_t nr = S.nloc_nb[d];
+                    const uint32_t lr = d == PN ? c.l - S.W + nr : c.l + S.W - S.nloc;
+                    outw[d] = (uint32_t)(((size_t)(d ^ 1u) * nr + lr) * 4u);
+                } else {
+                    outw[d] = (uint32_t)ll_index(S, 0, d ^ 1u, m, 0);
+                }
             }
             outi[d] = mi;
         }
@@ -216,15 +282,15 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
         bool busy = false;
         if (active) {
             unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
-            unsigned long long *const lln = S.ll + (size_t)nb1 * pstride;  // next cycle's
             // issue the boundary polls first (all four words of each slot)
             unsigned long long xa[4] = {0, 0, 0, 0}, xb[4] = {0, 0, 0, 0}, xc[4] = {0, 0, 0, 0},
                                xd[4] = {0, 0, 0, 0};
 #pragma unroll
             for (uint32_t d = 0; d < 4; ++d)
                 if ((ext >> d) & 1u) {
-                    ld_relaxed_x2(llp + inw[d], xa[d], xb[d]);
-                    ld_relaxed_x2(llp + inw[d] + 2, xc[d], xd[d]);
+                    const bool sys = (bedge >> d) & 1u;
+                    ll_load2(sys, llp + inw[d], xa[d], xb[d]);
+                    ll_load2(sys, llp + inw[d] + 2, xc[d], xd[d]);
                 }
 
             // deferred Phase 3 of cycle t-1
@@ -254,8 +320,9 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
                            ((uint32_t)(w0 >> 32) != LL_EMPTY &&
                             ((uint32_t)w1 != st || (uint32_t)w2 != st || (uint32_t)w3 != st))) {
                         if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
-                        ld_relaxed_x2(slot, w0, w1);
-                        ld_relaxed_x2(slot + 2, w2, w3);
+                        const bool sys = (bedge >> d) & 1u;
+                        ll_load2(sys, slot, w0, w1);
+                        ll_load2(sys, slot + 2, w2, w3);
                     }
                     const uint32_t x = (uint32_t)(w0 >> 32);
                     if ((uint32_t)w0 == st && x != LL_EMPTY) {
@@ -279,9 +346,10 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
             auto out = [&](uint32_t p, const Flit &f) {
                 const uint32_t slot = p ^ 1u;   // opp(p): N<->S (0,1), E<->W (2,3)
                 if ((ext >> p) & 1u) {
-                    unsigned long long *o = lln + pick4(outw, p);
-                    st_relaxed_x2(o + 2, llw(stn, f.z), llw(stn, f.w));
-                    st_relaxed_x2(o, llw(stn, f.x), llw(stn, f.y));
+                    const bool sys = (bedge >> p) & 1u;
+                    unsigned long long *o = ll_out(S, sys, p, nb1, pstride) + pick4(outw, p);
+                    ll_store2(sys, o + 2, llw(stn, f.z), llw(stn, f.w));
+                    ll_store2(sys, o, llw(stn, f.x), llw(stn, f.y));
                 } else {
                     const uint32_t so = (nb1 * 4u + slot) * np + pick4(outi, p);
                     sflit[so] = make_uint4(f.x, f.y, f.z, f.w);
@@ -326,7 +394,10 @@ k_tiled(Dev S, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activit
             const uint32_t idle_ext = ext & ~used;
 #pragma unroll
             for (uint32_t p = 0; p < 4; ++p)
-                if ((idle_ext >> p) & 1u) st_relaxed_u64(lln + outw[p], llw(stn, LL_EMPTY));
+                if ((idle_ext >> p) & 1u) {
+                    const bool sys = (bedge >> p) & 1u;
+                    ll_store1(sys, ll_out(S, sys, p, nb1, pstride) + outw[p], llw(stn, LL_EMPTY));
+                }
             if (has_ej) {
                 // while draining, quiescence is judged at the end of each cycle,
                 // so the service is not deferred there
@@ -425,9 +496,31 @@ size_t tiled_smem_bytes(const Dev &S, uint32_t np, bool with_hist)
     return (size_t)np * (9u * 16u + 8u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
 }
 
-// Pick TX x TY tiles (<= TILE_MIN_BLOCKS CTAs per SM, <= TILE_BLOCK_MAX nodes
-// each) minimising the largest tile, then its perimeter.
-cudaError_t tiled_configure(Dev &S, int device, uint32_t *grid, uint32_t *tpad, uint32_t *smem_hist)
+// Pick TX x TY tiles for one band (<= tiles_budget CTAs, <= TILE_BLOCK_MAX
+// nodes each) minimising the largest tile, then its perimeter.  Host only.
+bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
+{
+    uint64_t best_tn = ~0ull, best_per = ~0ull;
+    uint32_t bx = 0, by = 0;
+    for (uint32_t tx = 1; tx <= S.W && tx <= tiles_budget; ++tx) {
+        for (uint32_t ty = 1; ty <= S.rows && (uint64_t)tx * ty <= tiles_budget; ++ty) {
+            uint64_t tw = (S.W + tx - 1) / tx, th = (S.rows + ty - 1) / ty;
+            uint64_t tn = tw * th, per = tw + th;
+            if (tn < best_tn || (tn == best_tn && per < best_per)) { best_tn = tn; best_per = per; bx = tx; by = ty; }
+        }
+    }
+    if (bx == 0 || best_tn > TILE_BLOCK_MAX) return false;
+    S.TX = bx;
+    S.TY = by;
+    *tiles = bx * by;
+    *np = (uint32_t)((best_tn + 31u) / 32u * 32u);
+    return true;
+}
+
+// Shared-memory attribute and co-residency check for one launch of
+// total_tiles CTAs of np threads.
+cudaError_t tiled_prepare(uint32_t mode, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
+                          uint32_t *smem_hist)
 {
     int sms = 0, optin = 0, smem_sm = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -436,50 +529,38 @@ cudaError_t tiled_configure(Dev &S, int device, uint32_t *grid, uint32_t *tpad, 
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     if (e != cudaSuccess) return e;
-    const uint64_t max_ctas = (uint64_t)sms * TILE_MIN_BLOCKS;
-    uint64_t best_tn = ~0ull, best_per = ~0ull;
-    uint32_t bx = 0, by = 0;
-    for (uint32_t tx = 1; tx <= S.W && tx <= max_ctas; ++tx) {
-        for (uint32_t ty = 1; ty <= S.rows && (uint64_t)tx * ty <= max_ctas; ++ty) {
-            uint64_t tw = (S.W + tx - 1) / tx, th = (S.rows + ty - 1) / ty;
-            uint64_t tn = tw * th, per = tw + th;
-            if (tn < best_tn || (tn == best_tn && per < best_per)) { best_tn = tn; best_per = per; bx = tx; by = ty; }
-        }
-    }
-    if (best_tn > TILE_BLOCK_MAX) return cudaErrorInvalidConfiguration;
-    S.TX = bx;
-    S.TY = by;
-    const uint32_t np = (uint32_t)((best_tn + 31u) / 32u * 32u);
-    const void *fn = S.mode == 1u ? (const void *)k_tiled<1> : (const void *)k_tiled<0>;
+    Dev tmp;
+    tmp.nb = nb;
+    const void *fn = mode == 1u ? (const void *)k_tiled<1> : (const void *)k_tiled<0>;
     bool with_hist = true;
-    size_t smem = tiled_smem_bytes(S, np, true);
+    size_t smem = tiled_smem_bytes(tmp, np, true);
     if ((smem + 1024) * TILE_MIN_BLOCKS > (size_t)smem_sm || smem > (size_t)optin) {
         with_hist = false;
-        smem = tiled_smem_bytes(S, np, false);
+        smem = tiled_smem_bytes(tmp, np, false);
     }
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)np, smem);
     if (e != cudaSuccess) return e;
-    if ((uint64_t)per_sm * sms < (uint64_t)bx * by) return cudaErrorCooperativeLaunchTooLarge;
-    *grid = bx * by;
-    *tpad = np;
+    if ((uint64_t)per_sm * sms < total_tiles) return cudaErrorCooperativeLaunchTooLarge;
     *smem_hist = with_hist ? 1u : 0u;
     return cudaSuccess;
 }
 
-cudaError_t launch_tiled(const Dev &S, uint64_t t0, uint32_t ncyc, uint32_t grid, uint32_t tpad, uint32_t smem_hist,
-                         uint32_t *activity, cudaStream_t st)
+cudaError_t launch_ll_refresh(const Dev &S, uint64_t t0, cudaStream_t st)
 {
     k_ll_refresh<<<256, 256, 0, st>>>(S, t0);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    size_t smem = tiled_smem_bytes(S, tpad, smem_hist != 0);
-    Dev Sc = S;
-    void *args[] = {(void *)&Sc, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
-    const void *fn = S.mode == 1u ? (const void *)k_tiled<1> : (const void *)k_tiled<0>;
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(tpad), args, smem, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,
+                         uint32_t *activity, cudaStream_t st)
+{
+    size_t smem = tiled_smem_bytes(P.d[0], tpad, smem_hist != 0);
+    void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
+    const void *fn = P.d[0].mode == 1u ? (const void *)k_tiled<1> : (const void *)k_tiled<0>;
+    return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }
 
 cudaError_t launch_ll_reset(const Dev &S, uint64_t t, cudaStream_t st)

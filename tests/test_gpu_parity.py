@@ -226,3 +226,33 @@ def test_c3_drain_window(engine):
     for k in (37, 200):
         assert g.drain(k) == o.drain(k)
         assert_same(g, o)
+
+
+@pytest.mark.parametrize("bands", [2, 3, 5, 8])
+@pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
+def test_virtual_bands_match_oracle(bands, mode):
+    """Row bands (the multi-GPU partition, DESIGN 8) simulated on one GPU:
+    results identical to the oracle and to the unpartitioned run."""
+    cfg = (W.make(mesh_w=18, mesh_h=16, mode=mode, lam=0.3) if mode == W.MODE_UR
+           else W.lspd(22, 19, lam=0.2, mem_lat=30))
+    script = W.random_script(cfg, 400, 900, seed=11)
+    g = nb.NocSim(cfg, script=script, engine=nb.ENGINE_TILED, bands=bands)
+    o = Oracle(cfg, script=script)
+    for k in (1, 999, 600):
+        g.run(k)
+        o.run(k)
+    assert_same(g, o)
+    assert g.drain(50000) == o.drain(50000)
+    assert_same(g, o)
+    g.run(300)
+    o.run(300)
+    assert_same(g, o)
+
+
+def test_virtual_bands_c3():
+    cfg = W.c3()
+    g = nb.NocSim(cfg, bands=2)
+    o = Oracle(cfg)
+    g.run(1000)
+    o.run(1000)
+    assert_same(g, o)
