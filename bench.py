@@ -170,12 +170,18 @@ def run_ours(args):
         torch.cuda.set_device(local)
     dev = torch.cuda.current_device()
     desc, fn = WORKLOADS[args.workload]
-    # N > 1: independent replicas (distinct seeds) per GPU until the row-band
-    # engine is built: weak scaling, no data-path collective.
-    cfg = fn(seed=1 + rank)
-    n = cfg["mesh_w"] * cfg["mesh_h"]
     eng = {"auto": pkg.ENGINE_AUTO, "step": pkg.ENGINE_STEP, "persist": pkg.ENGINE_PERSIST, "tiled": pkg.ENGINE_TILED}[args.engine]
-    sim = pkg.NocSim(cfg, device=dev, engine=eng)
+    cfg = fn(seed=1)
+    if world > 1:
+        # weak scaling by row bands (DESIGN 8): the mesh grows to W x (H*N);
+        # rank r owns rows [r*H, (r+1)*H) and exchanges its edge rows' links
+        # with ranks r-1 / r+1 inside the kernel (CUDA IPC over NVLink)
+        from paper_1508_03235_b200 import dist as pdist
+        cfg["mesh_h"] = cfg["mesh_h"] * world
+        sim = pdist.create_band_sim(cfg, dev, engine=eng)
+    else:
+        sim = pkg.NocSim(cfg, device=dev, engine=eng)
+    n = sim.info()["nodes_local"]
     cyc = args.cycles_per_step
     l2buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if not args.no_flush else None
 
@@ -239,7 +245,10 @@ def run_ours(args):
                    "nodes_per_gpu": n, "cycles_per_step": cyc, "engine": info1["engine"],
                    "grid": info1["grid"], "block": info1["block"],
                    "l2_flush": "256 MiB buffer written between timed steps" if l2buf is not None else "none",
-                   "parallelism": "replicas x%d (distinct seeds)" % world if world > 1 else "single GPU"},
+                   "parallelism": ("row bands x%d (weak scaling: %dx%d mesh, one %d-row band per GPU, "
+                                   "in-kernel NVLink boundary exchange)" % (world, cfg["mesh_w"], cfg["mesh_h"],
+                                                                           cfg["mesh_h"] // world)
+                                   if world > 1 else "single GPU")},
         "e2e": {"value": n * cyc * e2e_steps * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": d2h,
                 "note": "noc_sim_run + noc_sim_stats per step, host wall clock; traffic is generated on "
@@ -252,7 +261,7 @@ def run_ours(args):
         "clocks": ck,
         "sim": {"hash": None, "drops": sum(v for k, v in delta.items() if k.startswith("drops_"))},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt = oracle_rate(cfg, args.cpu_cycles)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s cycles 0-%d from a fresh state, 1 host thread (%.1f s)" % (
