@@ -44,6 +44,7 @@ struct Acc {
 // Registers of one node for one cycle.
 struct NodeCtx {
     uint32_t l, n, x, y;
+    uint32_t deg;        // number of existing neighbours (router degree)
     uint32_t qctl;
     uint32_t hot;
     uint4 cold;
@@ -385,9 +386,10 @@ __device__ __forceinline__ uint32_t row_of(const Dev &S, uint32_t n) { return __
 // Returns the mask of output ports taken.
 // First choice of flit f at node c (eject at the destination, else the x-port
 // if dx != 0, else the y-port; PMDR P:L116), with the lifetime check (R32).
-__device__ __forceinline__ uint32_t first_choice(const Dev &S, const NodeCtx &c, const Flit &f, uint32_t t32)
+__device__ __forceinline__ uint32_t first_choice(const Dev &S, const NodeCtx &c, const Flit &f, uint32_t t32,
+                                                 uint32_t &bad)
 {
-    if (t32 - f.z > LIFE_MAX) atomicOr(S.err, ERR_AGE);
+    bad |= (t32 - f.z > LIFE_MAX) ? ERR_AGE : 0u;   // reported by the caller (R32)
     const uint32_t dst = f_dst(f);
     if (dst == c.n) return PX;
     const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
@@ -408,17 +410,18 @@ __device__ __forceinline__ uint32_t route(const Dev &S, const NodeCtx &c, Inputs
     // gives every flit its first choice whatever the ranking, and nothing is
     // deflected.
     {
-        uint32_t fc[5], seen = 0;
+        uint32_t fc[5], seen = 0, bad = 0;
         bool coll = false;
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
             fc[k] = PX;
             if ((in.present >> k) & 1u) {
-                fc[k] = first_choice(S, c, in.f[k], t32);
+                fc[k] = first_choice(S, c, in.f[k], t32, bad);
                 coll |= (seen >> fc[k]) & 1u;
                 seen |= 1u << fc[k];
             }
         }
+        if (bad) atomicOr(S.err, bad);
         if (!coll) {
             has_ej = false;
 #pragma unroll
@@ -556,9 +559,8 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
 __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t npresent, uint64_t t, Acc &acc,
                                             Flit &out)
 {
-    const uint32_t deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
     const uint32_t qn = q_count(c.qctl);
-    if (qn == 0u || npresent >= deg) return false;
+    if (qn == 0u || npresent >= c.deg) return false;
     const uint32_t h = q_head(c.qctl);
     uint32_t nx = q_next(c.qctl);
     if (!c.head_ok) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h]; c.head_ok = true; }
@@ -595,6 +597,7 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
     c.n = S.n0 + l;
     c.y = c.n / S.W;
     c.x = c.n - c.y * S.W;
+    c.deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
     c.qctl = S.fifo_ctl[l];
     c.hot = MODE == 1u ? S.core_hot[l] : 0u;
     c.head_ok = false;

@@ -167,7 +167,7 @@ __device__ __forceinline__ unsigned long long *ll_out(const Dev &S, bool band_ed
     return S.ll_nb[side] + (size_t)nb * 16u * S.nloc_nb[side];
 }
 
-template <uint32_t MODE>
+template <uint32_t MODE, bool DRAIN>
 __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
 {
@@ -181,7 +181,8 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     uint4 *sflit = smem4;
     uint4 *sinj = sflit + 8u * np;
     uint32_t *sst = reinterpret_cast<uint32_t *>(sinj + np);
-    unsigned int *scnt = sst + 8u * np;
+    uint32_t *snb = sst + 8u * np;                 // [4][np] neighbour node slot per port
+    unsigned int *scnt = snb + 4u * np;
     unsigned int *shist = smem_hist ? scnt + NCOUNTERS : nullptr;
     __shared__ int s_abort;
     __shared__ uint32_t s_busy[2];
@@ -209,13 +210,15 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     c.cold_loaded = true;
     c.q_dirty = c.hot_dirty = c.cold_dirty = false;
     c.busy_flit = false;
+    uint32_t errf = 0;     // overflow flags seen by this thread (R32), reported once
     c.qctl = 0u;
     c.hot = 0u;
     c.cold = make_uint4(0, 0, 0, 0);
     uint32_t ext = 0;      // bit d: port d crosses the tile boundary
     uint32_t intl = 0;     // bit d: port d exists inside the tile
     uint32_t bedge = 0;    // bit d: port d crosses the band edge (N: 0, S: 1)
-    uint32_t inw[4] = {0, 0, 0, 0}, outw[4] = {0, 0, 0, 0}, outi[4] = {0, 0, 0, 0};
+    uint32_t inw[4] = {0, 0, 0, 0}, outw[4] = {0, 0, 0, 0};
+    c.deg = 0;
     const uint32_t b0 = (uint32_t)t0 & 1u;
     if (active) {
         c.qctl = S.fifo_ctl[c.l];
@@ -229,6 +232,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         ext = ((lyy == 0 ? 1u : 0u) | (lyy + 1 == T.th ? 2u : 0u) | (lx + 1 == T.tw ? 4u : 0u) |
                (lx == 0 ? 8u : 0u)) & exist;
         intl = exist & ~ext;
+        c.deg = __popc(exist);
         bedge = ((c.y == S.row0 && c.y > 0) ? 1u : 0u) | ((c.y + 1 == S.row0 + S.rows && c.y + 1 < S.H) ? 2u : 0u);
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
@@ -250,7 +254,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     outw[d] = (uint32_t)ll_index(S, 0, d ^ 1u, m, 0);
                 }
             }
-            outi[d] = mi;
+            snb[d * np + i] = mi;
         }
         // internal inputs of cycle t0 (spilled by the previous launch)
         const uint32_t fl = S.flag[b0][c.l];
@@ -351,7 +355,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     ll_store2(sys, o + 2, llw(stn, f.z), llw(stn, f.w));
                     ll_store2(sys, o, llw(stn, f.x), llw(stn, f.y));
                 } else {
-                    const uint32_t so = (nb1 * 4u + slot) * np + pick4(outi, p);
+                    const uint32_t so = (nb1 * 4u + slot) * np + snb[p * np + i];
                     sflit[so] = make_uint4(f.x, f.y, f.z, f.w);
                     sst[so] = stn;
                 }
@@ -366,7 +370,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 bool coll = false;
                 for (uint32_t m = present; m; m &= m - 1u) {
                     const uint32_t k = __ffs(m) - 1u;
-                    const uint32_t fc = first_choice(S, c, slot_flit(k), st);
+                    const uint32_t fc = first_choice(S, c, slot_flit(k), st, errf);
                     coll |= (seen >> fc) & 1u;
                     seen |= 1u << fc;
                     fcs |= fc << (4u * k);
@@ -401,19 +405,19 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             if (has_ej) {
                 // while draining, quiescence is judged at the end of each cycle,
                 // so the service is not deferred there
-                if (activity) phase3(S, K, c, ej, t, acc);
+                if (DRAIN) phase3(S, K, c, ej, t, acc);
                 else { pend = ej; has_pend = true; if (MODE == 1u) prefetch_service(S, c, ej); }
             }
-            busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
+            if (DRAIN) busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
             // the generation draw of cycle t+1, off the critical path
             predraw(S, c, t + 1);
         }
         // The cycle barrier is a full BAR.SYNC: it orders this cycle's shared-
         // memory link stores before the next cycle's loads (a reducing barrier,
         // __syncthreads_or, measurably did not on sm_100a).
-        if (activity && busy) s_busy[cc & 1u] = cc + 1u;
+        if (DRAIN && busy) s_busy[cc & 1u] = cc + 1u;
         __syncthreads();
-        if (activity && i == 0 && s_busy[cc & 1u] == cc + 1u) atomicAdd(&activity[cc], 1u);
+        if (DRAIN && i == 0 && s_busy[cc & 1u] == cc + 1u) atomicAdd(&activity[cc], 1u);
         if (s_abort) break;
     }
 
@@ -421,6 +425,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     const uint64_t tend = t0 + ncyc;
     if (active) {
         if (has_pend) phase3(S, K, c, pend, tend - 1, acc);
+        if (errf) atomicOr(S.err, errf);
         S.fifo_ctl[c.l] = c.qctl;
         if (MODE == 1u) {
             S.core_hot[c.l] = c.hot;
@@ -493,7 +498,7 @@ __global__ void k_ll_reset(Dev S, uint64_t t)
 // ------------------------------------------------------------------ host side
 size_t tiled_smem_bytes(const Dev &S, uint32_t np, bool with_hist)
 {
-    return (size_t)np * (9u * 16u + 8u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
+    return (size_t)np * (9u * 16u + 12u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
 }
 
 // Pick TX x TY tiles for one band (<= tiles_budget CTAs, <= TILE_BLOCK_MAX
@@ -531,19 +536,22 @@ cudaError_t tiled_prepare(uint32_t mode, uint32_t nb, uint32_t np, uint32_t tota
     if (e != cudaSuccess) return e;
     Dev tmp;
     tmp.nb = nb;
-    const void *fn = mode == 1u ? (const void *)k_tiled<1> : (const void *)k_tiled<0>;
     bool with_hist = true;
     size_t smem = tiled_smem_bytes(tmp, np, true);
     if ((smem + 1024) * TILE_MIN_BLOCKS > (size_t)smem_sm || smem > (size_t)optin) {
         with_hist = false;
         smem = tiled_smem_bytes(tmp, np, false);
     }
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)np, smem);
-    if (e != cudaSuccess) return e;
-    if ((uint64_t)per_sm * sms < total_tiles) return cudaErrorCooperativeLaunchTooLarge;
+    const void *fns[2] = {mode == 1u ? (const void *)k_tiled<1, false> : (const void *)k_tiled<0, false>,
+                          mode == 1u ? (const void *)k_tiled<1, true> : (const void *)k_tiled<0, true>};
+    for (const void *fn : fns) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)np, smem);
+        if (e != cudaSuccess) return e;
+        if ((uint64_t)per_sm * sms < total_tiles) return cudaErrorCooperativeLaunchTooLarge;
+    }
     *smem_hist = with_hist ? 1u : 0u;
     return cudaSuccess;
 }
@@ -559,7 +567,9 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
 {
     size_t smem = tiled_smem_bytes(P.d[0], tpad, smem_hist != 0);
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
-    const void *fn = P.d[0].mode == 1u ? (const void *)k_tiled<1> : (const void *)k_tiled<0>;
+    const bool dr = activity != nullptr;
+    const void *fn = P.d[0].mode == 1u ? (dr ? (const void *)k_tiled<1, true> : (const void *)k_tiled<1, false>)
+                                       : (dr ? (const void *)k_tiled<0, true> : (const void *)k_tiled<0, false>);
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }
 
