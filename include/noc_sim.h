@@ -54,6 +54,7 @@ extern "C" {
 #define NOC_ENGINE_STEP     1u  /* one fused node-step launch per cycle           */
 #define NOC_ENGINE_PERSIST  2u  /* persistent kernel, neighbour-progress sync     */
 #define NOC_ENGINE_TILED    3u  /* persistent kernel, tiles in shared memory      */
+#define NOC_ENGINE_TILED4   4u  /* as TILED, 4 lanes (one per router port) per node */
 
 /* A scripted generation event (golden tests; trace replay).
  * At each generation opportunity of node `node` at cycle t (every cycle in UR

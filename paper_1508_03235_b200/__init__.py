@@ -26,7 +26,7 @@ COUNTER_NAMES = (
 KIND_NAMES = ("probe", "da", "dr", "ndr", "rq", "ra", "trap", "ev")
 
 NOC_OK, NOC_EINVAL, NOC_ENOMEM, NOC_ECUDA, NOC_ENCCL, NOC_EOVERFLOW, NOC_ESTATE = 0, -1, -2, -3, -4, -5, -6
-ENGINE_AUTO, ENGINE_STEP, ENGINE_PERSIST, ENGINE_TILED = 0, 1, 2, 3
+ENGINE_AUTO, ENGINE_STEP, ENGINE_PERSIST, ENGINE_TILED, ENGINE_TILED4 = 0, 1, 2, 3, 4
 
 
 class noc_sim_event(C.Structure):

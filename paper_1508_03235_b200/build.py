@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnocsim.so")
-SOURCES = ["kernels.cu", "tile_engine.cu", "runtime.cu"]
+SOURCES = ["kernels.cu", "tile_engine.cu", "tile4_engine.cu", "runtime.cu"]
 HEADERS = ["common.cuh", "node_logic.cuh", "kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -26,6 +26,16 @@ cudaError_t tiled_prepare(uint32_t mode, uint32_t nb, uint32_t np, uint32_t tota
 cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,
                          uint32_t *activity, cudaStream_t st);
 cudaError_t launch_ll_refresh(const Dev &S, uint64_t t0, cudaStream_t st);
+
+// TILED4 engine (tile4_engine.cu): 4 lanes per node, <= 160 nodes per CTA,
+// 2 CTAs per SM
+constexpr uint32_t TILE4_BLOCK_MAX = 640;
+constexpr uint32_t TILE4_MIN_BLOCKS = 2;
+bool tiled4_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np);
+cudaError_t tiled4_prepare(uint32_t mode, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
+                           uint32_t *smem_hist);
+cudaError_t launch_tiled4(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t np, uint32_t smem_hist,
+                          uint32_t *activity, cudaStream_t st);
 cudaError_t launch_ll_reset(const Dev &S, uint64_t t, cudaStream_t st);
 
 cudaError_t launch_step(const Dev &S, uint64_t t, uint32_t *activity, cudaStream_t st);

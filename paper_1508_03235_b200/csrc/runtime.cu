@@ -128,7 +128,7 @@ static int validate(const noc_sim_config *c)
         return fail(NOC_EINVAL, "world_size must be <= 8 and <= mesh_h");
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
-    if (c->engine > NOC_ENGINE_TILED) return fail(NOC_EINVAL, "unknown engine");
+    if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
     for (int i = 0; i < 7; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->n_script && !c->script) return fail(NOC_EINVAL, "n_script > 0 with a null script");
@@ -336,35 +336,42 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     // engine: TILED when every band's tiles fit one CTA of <= TILE_BLOCK_MAX
     // threads per SM, else PERSIST (DESIGN 6.2); bands require TILED
     s->engine = cfg->engine;
-    if (s->P > 1 && s->engine != NOC_ENGINE_AUTO && s->engine != NOC_ENGINE_TILED)
-        return bail(fail(NOC_EINVAL, "row bands need the TILED engine"));
-    if (s->engine == NOC_ENGINE_AUTO || s->engine == NOC_ENGINE_TILED) {
+    if (s->P > 1 && s->engine != NOC_ENGINE_AUTO && s->engine != NOC_ENGINE_TILED && s->engine != NOC_ENGINE_TILED4)
+        return bail(fail(NOC_EINVAL, "row bands need a TILED engine"));
+    // AUTO tries TILED4 (4 lanes per node, 2 CTAs per SM), then TILED, then PERSIST
+    for (uint32_t cand : {NOC_ENGINE_TILED4, NOC_ENGINE_TILED}) {
+        if (!(s->engine == NOC_ENGINE_AUTO || s->engine == cand)) continue;
+        const bool four = cand == NOC_ENGINE_TILED4;
         bool ok = true;
-        uint32_t np = 32, total = 0;
-        const uint32_t budget = std::max<uint32_t>(1u, (uint32_t)s->sm_count / (uint32_t)s->nb);
+        uint32_t np = four ? 8 : 32, total = 0;
+        const uint32_t per_sm = four ? TILE4_MIN_BLOCKS : TILE_MIN_BLOCKS;
+        const uint32_t budget = std::max<uint32_t>(1u, (uint32_t)s->sm_count * per_sm / (uint32_t)s->nb);
         s->set.nbands = (uint32_t)s->nb;
         s->set.tile0[0] = 0;
         for (int k = 0; k < s->nb && ok; ++k) {
             uint32_t tiles = 0, npk = 0;
-            ok = tiled_plan(s->D[k], budget, &tiles, &npk);
+            ok = four ? tiled4_plan(s->D[k], budget, &tiles, &npk) : tiled_plan(s->D[k], budget, &tiles, &npk);
             np = std::max(np, npk);
             total += tiles;
             s->set.tile0[k + 1] = total;
         }
-        cudaError_t ce = ok ? tiled_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
-                            : cudaErrorInvalidConfiguration;
+        cudaError_t ce = cudaErrorInvalidConfiguration;
+        if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
+                          : tiled_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {
-            s->engine = NOC_ENGINE_TILED;
+            s->engine = cand;
             s->t_tpad = np;
-        } else {
-            cudaGetLastError();
-            if (s->engine == NOC_ENGINE_TILED || s->P > 1)
-                return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") +
-                                                 cudaGetErrorString(ce)));
-            s->engine = NOC_ENGINE_PERSIST;
+            break;
         }
+        cudaGetLastError();
+        if (s->engine == cand)
+            return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") + cudaGetErrorString(ce)));
     }
-    if (s->engine == NOC_ENGINE_TILED) {
+    if (s->engine == NOC_ENGINE_AUTO) {
+        if (s->P > 1) return bail(fail(NOC_EINVAL, "row bands do not fit a TILED engine"));
+        s->engine = NOC_ENGINE_PERSIST;
+    }
+    if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
         for (int k = 0; k < s->nb; ++k)
             if ((rc = dalloc(s, &s->D[k].ll, (size_t)32u * s->D[k].nloc))) return bail(rc);
         // neighbour bands' boundary slots
@@ -422,13 +429,15 @@ static void set_gen(noc_sim *s, uint32_t gen)
 static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
 {
     cudaError_t e;
-    if (s->engine == NOC_ENGINE_TILED) {
+    if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
             for (int b = 0; b < s->nb; ++b) CU(launch_ll_refresh(s->D[b], s->t + done, s->stream));
-            e = launch_tiled(s->set, s->t + done, k, s->t_tpad, s->t_smem_hist, activity ? activity + done : nullptr,
-                             s->stream);
+            uint32_t *act = activity ? activity + done : nullptr;
+            e = s->engine == NOC_ENGINE_TILED4
+                    ? launch_tiled4(s->set, s->t + done, k, s->t_tpad, s->t_smem_hist, act, s->stream)
+                    : launch_tiled(s->set, s->t + done, k, s->t_tpad, s->t_smem_hist, act, s->stream);
             if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(e));
             // ranks: the next refresh may only run once the neighbours stopped
             // writing into this band's boundary slots
@@ -521,7 +530,7 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
             s->t = t0 + k;
             // boundary slots were stamped up to the end of the chunk: re-stamp
             // them EMPTY for the rewound cycle (nothing is in flight)
-            if (s->engine == NOC_ENGINE_TILED)
+            if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4)
                 for (int b = 0; b < s->nb; ++b) CU(launch_ll_reset(s->D[b], s->t, s->stream));
             if ((rc = allreduce_u32(s, s->d_scratch + DRAIN_CHUNK, 1))) return rc;
         } else {
@@ -606,9 +615,9 @@ extern "C" int noc_sim_get_info(noc_sim *s, noc_sim_info *o)
     if (!s || !o) return fail(NOC_EINVAL, "null argument");
     memset(o, 0, sizeof *o);
     o->engine = s->engine;
-    if (s->engine == NOC_ENGINE_TILED) {
+    if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
         o->grid = s->set.tile0[s->set.nbands];
-        o->block = s->t_tpad;
+        o->block = s->engine == NOC_ENGINE_TILED4 ? 4u * s->t_tpad : s->t_tpad;
         o->reserved[0] = (int32_t)s->D[0].TX;
         o->reserved[1] = (int32_t)s->D[0].TY;
     } else if (s->engine == NOC_ENGINE_PERSIST) {

@@ -15,7 +15,8 @@ from oracle import Oracle
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = [nb.ENGINE_STEP, nb.ENGINE_PERSIST, nb.ENGINE_TILED]
+ENGINES = [nb.ENGINE_STEP, nb.ENGINE_PERSIST, nb.ENGINE_TILED, nb.ENGINE_TILED4]
+TILED_ENGINES = [nb.ENGINE_TILED, nb.ENGINE_TILED4]
 
 
 def both(cfg, cycles, engine=nb.ENGINE_AUTO, script=None, drain=None, split=None):
@@ -187,17 +188,18 @@ def test_c3_long_run_properties():
 def test_auto_engine_is_tiled_at_bench_size():
     g = nb.NocSim(W.c3())
     info = g.info()
-    assert info["engine"] == nb.ENGINE_TILED and info["grid"] <= 2 * info["sm_count"]
+    assert info["engine"] in TILED_ENGINES and info["grid"] <= 2 * info["sm_count"]
 
 
+@pytest.mark.parametrize("engine", TILED_ENGINES)
 @pytest.mark.parametrize("w,h", [(13, 11), (148, 2), (2, 300), (31, 29)])
-def test_tiled_odd_tilings(w, h):
+def test_tiled_odd_tilings(w, h, engine):
     """Tilings with 1-wide tiles, single-row bands and ragged tile sizes."""
     cfg = W.make(mesh_w=w, mesh_h=h, mode=W.MODE_LSPD, lam=0.3, sendq_cap=32, l2_sets=4, mem_lat=20)
-    g, o = both(cfg, 1500, nb.ENGINE_TILED)
+    g, o = both(cfg, 1500, engine)
     assert_same(g, o)
     cfg = W.make(mesh_w=w, mesh_h=h, mode=W.MODE_UR, lam=0.2)
-    g, o = both(cfg, 1500, nb.ENGINE_TILED)
+    g, o = both(cfg, 1500, engine)
     assert_same(g, o)
 
 
@@ -228,15 +230,16 @@ def test_c3_drain_window(engine):
         assert_same(g, o)
 
 
+@pytest.mark.parametrize("engine", TILED_ENGINES)
 @pytest.mark.parametrize("bands", [2, 3, 5, 8])
 @pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
-def test_virtual_bands_match_oracle(bands, mode):
+def test_virtual_bands_match_oracle(bands, mode, engine):
     """Row bands (the multi-GPU partition, DESIGN 8) simulated on one GPU:
     results identical to the oracle and to the unpartitioned run."""
     cfg = (W.make(mesh_w=18, mesh_h=16, mode=mode, lam=0.3) if mode == W.MODE_UR
            else W.lspd(22, 19, lam=0.2, mem_lat=30))
     script = W.random_script(cfg, 400, 900, seed=11)
-    g = nb.NocSim(cfg, script=script, engine=nb.ENGINE_TILED, bands=bands)
+    g = nb.NocSim(cfg, script=script, engine=engine, bands=bands)
     o = Oracle(cfg, script=script)
     for k in (1, 999, 600):
         g.run(k)
