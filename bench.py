@@ -28,6 +28,8 @@ sys.path.insert(0, ROOT)
 from paper_1508_03235_b200 import workloads as W  # noqa: E402
 
 METRIC = "simulated node-cycles/sec (device-timed) at 1/2/4/8 B200; % of HBM roofline"
+ENGINES = {"auto": 0, "step": 1, "persist": 2, "tiled": 3, "tiled4": 4}          # NOC_ENGINE_*
+KERNELS = {1: "k_step", 2: "k_persist", 3: "k_tiled", 4: "k_tiled4"}
 UNIT = "node-cycles/s"
 WORKLOADS = {
     "c3": ("208x208 LSPD (BASELINE configs[2], paper's largest mesh)", W.c3),
@@ -170,7 +172,7 @@ def run_ours(args):
         torch.cuda.set_device(local)
     dev = torch.cuda.current_device()
     desc, fn = WORKLOADS[args.workload]
-    eng = {"auto": pkg.ENGINE_AUTO, "step": pkg.ENGINE_STEP, "persist": pkg.ENGINE_PERSIST, "tiled": pkg.ENGINE_TILED}[args.engine]
+    eng = ENGINES[args.engine]
     cfg = fn(seed=1)
     if world > 1:
         # weak scaling by row bands (DESIGN 8): the mesh grows to W x (H*N);
@@ -256,7 +258,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": {1: "k_step", 2: "k_persist", 3: "k_tiled"}[info1["engine"]],
+                     "kernel": KERNELS.get(info1["engine"], "engine %d" % info1["engine"]),
                      "bytes_per_node_cycle": B, "rates": rates, "per_launch_ms": per_launch_ms},
         "clocks": ck,
         "sim": {"hash": None, "drops": sum(v for k, v in delta.items() if k.startswith("drops_"))},
@@ -284,7 +286,7 @@ def main():
     ap.add_argument("--cycles-per-step", type=int, default=2000)
     ap.add_argument("--ref-cycles-per-step", type=int, default=200)
     ap.add_argument("--cpu-cycles", type=int, default=2000)
-    ap.add_argument("--engine", default="auto", choices=["auto", "step", "persist", "tiled"])
+    ap.add_argument("--engine", default="auto", choices=sorted(ENGINES))
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
