@@ -14,7 +14,9 @@ import os
 from . import workloads  # noqa: F401  (seeded configs)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnocsim.so")
+# NOCSIM_LIB selects another in-tree build of the same library (A/B timing
+# of kernel variants, tools/); default: the one build() writes
+LIB_PATH = os.environ.get("NOCSIM_LIB") or os.path.join(_HERE, "libnocsim.so")
 
 COUNTER_NAMES = (
     "generated", "packets_enqueued", "injected", "ejected", "hops", "deflections",

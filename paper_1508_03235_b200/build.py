@@ -12,13 +12,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libnocsim.so")
+LIB = os.environ.get("NOCSIM_LIB") or os.path.join(HERE, "libnocsim.so")
 SOURCES = ["kernels.cu", "tile_engine.cu", "tile4_engine.cu", "runtime.cu"]
 HEADERS = ["common.cuh", "node_logic.cuh", "kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+# extra -D flags for kernel-variant A/B builds (tools/); none by default
+FLAGS += os.environ.get("NOCSIM_DEFS", "").split()
 
 
 def _stale(out, deps):
@@ -33,7 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps.append(os.path.join(ROOT, "include", "noc_sim.h"))
     if not force and not _stale(LIB, deps):
         return LIB
-    objdir = os.path.join(HERE, "_build")
+    objdir = os.path.join(HERE, "_build", os.path.basename(LIB))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in SOURCES:

@@ -245,19 +245,24 @@ __device__ __forceinline__ bool script_next(const Dev &S, const NodeCtx &c, uint
 // ---------------------------------------------------------------------------
 // The Philox draw of node n for cycle t (R25): fire flag and value (UR: probe
 // destination; LSPD: block tag, DESIGN 3.3).
+// The value of a firing draw r1..r3 of node n (UR: probe destination; LSPD:
+// block tag, DESIGN 3.3)
+__device__ __forceinline__ uint32_t draw_value(const Dev &S, uint32_t n, uint32_t r1, uint32_t r2, uint32_t r3)
+{
+    if (S.mode == 0u) {
+        uint32_t d = mulhi32(r1, S.N - 1u);
+        return d + (d >= n);
+    }
+    if (r1 < S.thr_priv) return n * S.tpn + mulhi32(r2, S.priv);
+    return mulhi32(r2, S.N) * S.tpn + S.priv + mulhi32(r3, S.tpn - S.priv);
+}
+
 __device__ __forceinline__ bool draw(const Dev &S, const NodeCtx &c, uint64_t t, uint32_t &val)
 {
     uint32_t r[4];
     philox4x32_10(S.seed_lo, S.seed_hi, c.n, (uint32_t)t, (uint32_t)(t >> 32), 0u, r);
     if (r[0] >= S.thr_inj) return false;
-    if (S.mode == 0u) {
-        uint32_t d = mulhi32(r[1], S.N - 1u);
-        val = d + (d >= c.n);
-    } else if (r[1] < S.thr_priv) {
-        val = c.n * S.tpn + mulhi32(r[2], S.priv);
-    } else {
-        val = mulhi32(r[2], S.N) * S.tpn + S.priv + mulhi32(r[3], S.tpn - S.priv);
-    }
+    val = draw_value(S, c.n, r[1], r[2], r[3]);
     return true;
 }
 
@@ -345,6 +350,41 @@ __device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx
             fire = true; T = v;
         } else {
             fire = draw_now(S, c, t, T);
+        }
+        if (fire) start_access(S, K, c, T, t);
+    }
+}
+
+// Phase 1 (LSPD) with the generation draws taken from a window computed ahead
+// by the whole warp (TILED engine): bit k of wmask says whether the draw of
+// cycle wbase+k fires (r0 < thr_inj); the value of the window's first firing
+// draw is cached in nd_val.  Outside a window the draw is computed here.  The
+// model is phase1_lspd's; only where the Philox evaluations run differs.
+__device__ __forceinline__ void phase1_lspd_win(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t,
+                                                uint32_t wbase, uint32_t wmask)
+{
+    uint32_t mode = core_mode(c.hot);
+    if ((mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {
+        if (mode == MMEMWAIT) {
+            load_cold(S, c);
+            if (c.cold.w & 1u) install(S, K, c, c.cold.z, t);
+        }
+        complete(S, K, c, t);
+        mode = MIDLE;
+    }
+    if (mode == MIDLE && S.gen) {
+        uint32_t v, T = 0;
+        bool fire = false;
+        const uint32_t k = (uint32_t)t - wbase;
+        if (S.has_script && script_next(S, c, t, v)) {
+            fire = true; T = v;
+        } else if (k < 32u) {
+            if ((wmask >> k) & 1u) {
+                if (c.nd_ok && c.nd_t == (uint32_t)t) { T = c.nd_val; fire = true; }
+                else fire = draw(S, c, t, T);
+            }
+        } else {
+            fire = draw(S, c, t, T);
         }
         if (fire) start_access(S, K, c, T, t);
     }

@@ -61,6 +61,20 @@ __device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t p)
     return p == 0u ? a[0] : p == 1u ? a[1] : p == 2u ? a[2] : a[3];
 }
 
+// Predicated shared-memory stores (no branch around them)
+__device__ __forceinline__ void sts128_if(bool c, uint4 *p, const Flit &v)
+{
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n\t}"
+                 ::"r"((uint32_t)c), "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void sts8_if(bool c, uint8_t *p)
+{
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u8 [%1], %2;\n\t}"
+                 ::"r"((uint32_t)c), "r"(a), "r"(1u) : "memory");
+}
+
 struct TileShape {
     uint32_t x0, y0, tw, th, tn;
 };
@@ -109,12 +123,6 @@ __device__ __forceinline__ uint32_t tile_slot(const TileShape &T, uint32_t lx, u
     return ic + 2 * T.tw + (T.th - 2) + (ly - 1);
 }
 
-// Dynamic shared memory layout (np = blockDim.x node slots):
-//   uint4    sflit[2][4][np]   link flits (input slot d of node slot i, by parity)
-//   uint32_t sst[2][4][np]     stamp = the cycle the slot is an input of
-//   uint4    sinj[np]          the flit injected this cycle
-//   uint32_t scnt[NCOUNTERS]
-//   uint32_t shist[3][nb]      (optional)
 __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long *p)
 {
     unsigned long long v;
@@ -167,10 +175,68 @@ __device__ __forceinline__ unsigned long long *ll_out(const Dev &S, bool band_ed
     return S.ll_nb[side] + (size_t)nb * 16u * S.nloc_nb[side];
 }
 
+// Dynamic shared memory layout (np = blockDim.x node slots):
+//   uint4    sflit[2][4][np]   link flits (input slot d of node slot i, by parity)
+//   uint32_t sfl[2][np]        occupancy word of node slot i: byte d is 1 iff
+//                              input slot d holds a flit.  The receiver clears
+//                              its word when it reads it; the next writes to
+//                              that parity come a cycle later, after the cycle
+//                              barrier, so no stamp (and no ABA) is needed
+//   uint32_t scnt[NCOUNTERS]
+//   uint32_t shist[3][nb]      (optional)
+//
+// The cycle body is written for few instructions per warp: 32 nodes share a
+// warp, so any per-node branch costs the warp its full length whenever one
+// lane takes it.  Hence (i) the occupancy of all four slots is one shared
+// load, (ii) the routing decision of the common case is a handful of
+// predicated operations per present flit, and the general case (two flits
+// want the same port) works on packed 8-bit port preferences and ranks from a
+// 6-comparison tournament, (iii) the LSPD generation draws (one Philox4x32-10
+// per idle node-cycle, DESIGN 3.3) are evaluated 32 cycles at a time by the
+// whole warp, one lane per cycle, instead of by one lane per cycle.
+// Per-warp cycle trace (tools/trace_tiled.py; built only with -DNOC_TRACE):
+// for each traced cycle and warp, the cycle-start clock, the clock offsets at
+// which the boundary inputs were complete and the warp reached the cycle
+// barrier, and the OR of its lanes' event bits (1 deferred Phase 3, 2 Phase-1
+// state change, 4 Phase-1 enqueue, 8 draw-window refresh, 16 port conflict,
+// 32 injection, 64 flits present, 128 boundary node).
+#ifdef NOC_TRACE
+constexpr uint32_t TRACE_CYC = 1024, TRACE_WARPS = 1536;
+__device__ uint4 g_trace[TRACE_CYC][TRACE_WARPS];
+__device__ int g_trace_on;
+#define TRACE_DECL long long tr_c0 = clock64(), tr_x = 0; uint32_t tr_ev = 0, tr_h = 0, tr_q = 0;
+#define TRACE_EV(b) tr_ev |= (b);
+#define TRACE_P1_BEGIN tr_h = c.hot; tr_q = c.qctl;
+#define TRACE_P1_END tr_ev |= (c.hot != tr_h ? 2u : 0u) | (c.qctl != tr_q ? 4u : 0u);
+#define TRACE_EXT_DONE tr_x = clock64();
+#define TRACE_END                                                                                       \
+    {                                                                                                   \
+        const uint32_t ev = __reduce_or_sync(0xFFFFFFFFu, tr_ev);                                       \
+        const long long tr_a = clock64();                                                               \
+        const uint32_t xw = __reduce_max_sync(0xFFFFFFFFu, tr_x ? (uint32_t)(tr_x - tr_c0) : 0u);       \
+        const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);                        \
+        if (g_trace_on && (threadIdx.x & 31u) == 0u && cc < TRACE_CYC && wg < TRACE_WARPS)              \
+            g_trace[cc][wg] = make_uint4((uint32_t)tr_c0, (uint32_t)(tr_a - tr_c0), ev, xw);            \
+    }
+extern "C" int noc_trace_ctl(int on, void *host, size_t bytes)
+{
+    if (host) return (int)cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace));
+    return (int)cudaMemcpyToSymbol(g_trace_on, &on, sizeof(int));
+}
+#else
+#define TRACE_DECL
+#define TRACE_EV(b)
+#define TRACE_P1_BEGIN
+#define TRACE_P1_END
+#define TRACE_EXT_DONE
+#define TRACE_END
+#endif
+
 template <uint32_t MODE, bool DRAIN>
 __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
 {
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
     // this CTA's band and tile
     uint32_t band = 0;
     while (band + 1 < P.nbands && blockIdx.x >= P.tile0[band + 1]) ++band;
@@ -179,15 +245,13 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     extern __shared__ uint4 smem4[];
     const uint32_t np = blockDim.x;
     uint4 *sflit = smem4;
-    uint4 *sinj = sflit + 8u * np;
-    uint32_t *sst = reinterpret_cast<uint32_t *>(sinj + np);
-    uint32_t *snb = sst + 8u * np;                 // [4][np] neighbour node slot per port
-    unsigned int *scnt = snb + 4u * np;
+    uint32_t *sfl = reinterpret_cast<uint32_t *>(sflit + 8u * np);
+    unsigned int *scnt = sfl + 2u * np;
     unsigned int *shist = smem_hist ? scnt + NCOUNTERS : nullptr;
     __shared__ int s_abort;
     __shared__ uint32_t s_busy[2];
 
-    const uint32_t i = threadIdx.x;
+    const uint32_t i = threadIdx.x, lane = i & 31u;
     const TileShape T = tile_shape(S, tile);
     const bool active = i < T.tn;
 
@@ -207,6 +271,8 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     c.l = c.n - S.n0;
     c.head_ok = false;
     c.nd_ok = false;
+    c.nd_t = 0u;
+    c.nd_val = 0u;
     c.cold_loaded = true;
     c.q_dirty = c.hot_dirty = c.cold_dirty = false;
     c.busy_flit = false;
@@ -214,10 +280,12 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     c.qctl = 0u;
     c.hot = 0u;
     c.cold = make_uint4(0, 0, 0, 0);
+    uint32_t exist = 0;    // bit d: port d has a neighbour
     uint32_t ext = 0;      // bit d: port d crosses the tile boundary
     uint32_t intl = 0;     // bit d: port d exists inside the tile
     uint32_t bedge = 0;    // bit d: port d crosses the band edge (N: 0, S: 1)
     uint32_t inw[4] = {0, 0, 0, 0}, outw[4] = {0, 0, 0, 0};
+    uint32_t nbr01 = 0, nbr23 = 0;   // neighbour node slot of ports N,S / E,W (16 bits each)
     c.deg = 0;
     const uint32_t b0 = (uint32_t)t0 & 1u;
     if (active) {
@@ -227,8 +295,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             c.cold = S.core_cold[c.l];
         }
         if (q_count(c.qctl)) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + q_head(c.qctl)]; c.head_ok = true; }
-        const uint32_t exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) |
-                               (c.x > 0 ? 8u : 0u);
+        exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) | (c.x > 0 ? 8u : 0u);
         ext = ((lyy == 0 ? 1u : 0u) | (lyy + 1 == T.th ? 2u : 0u) | (lx + 1 == T.tw ? 4u : 0u) |
                (lx == 0 ? 8u : 0u)) & exist;
         intl = exist & ~ext;
@@ -254,22 +321,59 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     outw[d] = (uint32_t)ll_index(S, 0, d ^ 1u, m, 0);
                 }
             }
-            snb[d * np + i] = mi;
+            if (d < 2u) nbr01 |= mi << (16u * d);
+            else nbr23 |= mi << (16u * (d - 2u));
         }
         // internal inputs of cycle t0 (spilled by the previous launch)
         const uint32_t fl = S.flag[b0][c.l];
         const uint8_t s0 = stamp_of(t0);
+        uint32_t occ = 0;
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
-            const uint32_t si = (b0 * 4u + d) * np + i;
-            bool has = false;
             if (((intl >> d) & 1u) && ((fl >> (8u * d)) & 0xFFu) == s0) {
-                sflit[si] = S.flit[b0][(size_t)d * S.nloc + c.l];
-                has = true;
+                sflit[(b0 * 4u + d) * np + i] = S.flit[b0][(size_t)d * S.nloc + c.l];
+                occ |= 1u << (8u * d);
             }
-            sst[si] = has ? (uint32_t)t0 : (uint32_t)t0 - 1u;
-            sst[((b0 ^ 1u) * 4u + d) * np + i] = (uint32_t)t0 - 1u;
         }
+        sfl[b0 * np + i] = occ;
+        sfl[(b0 ^ 1u) * np + i] = 0u;
+    }
+
+    // Draw window (LSPD): bit k of wmask = the draw of cycle wbase+k fires.
+    // Lanes that need a window for cycle tn (idle, or possibly idle by then)
+    // get one: the warp evaluates the 32 draws of one requester at a time.
+    uint32_t wbase = (uint32_t)t0 - 64u, wmask = 0u;
+    auto refresh = [&](bool need, uint64_t tn) {
+        uint32_t nm = __ballot_sync(FULL, need);
+        while (nm) {
+            const uint32_t j = __ffs(nm) - 1u;
+            nm &= nm - 1u;
+            const uint32_t nj = __shfl_sync(FULL, c.n, j);
+            const uint64_t tk = tn + lane;
+            uint32_t r[4];
+            philox4x32_10(S.seed_lo, S.seed_hi, nj, (uint32_t)tk, (uint32_t)(tk >> 32), 0u, r);
+            const uint32_t m = __ballot_sync(FULL, r[0] < S.thr_inj);
+            const uint32_t src = m ? __ffs(m) - 1u : 0u;
+            const uint32_t r1 = __shfl_sync(FULL, r[1], src);
+            const uint32_t r2 = __shfl_sync(FULL, r[2], src);
+            const uint32_t r3 = __shfl_sync(FULL, r[3], src);
+            if (lane == j) {
+                wbase = (uint32_t)tn;
+                wmask = m;
+                c.nd_ok = m != 0u;
+                if (m) {
+                    c.nd_t = (uint32_t)tn + src;
+                    c.nd_val = draw_value(S, c.n, r1, r2, r3);
+                    prefetch_l1(set_ptr(S, c, c.nd_val));
+                }
+            }
+        }
+    };
+    const bool windows = MODE == 1u && S.gen && !S.has_script;
+    if (windows) {
+        const uint32_t mode = core_mode(c.hot);
+        const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t0) & 0x1FFFFFFFu) == 0u);
+        refresh(active && (mode == MIDLE || expiring), t0);
     }
     __syncthreads();
 
@@ -284,6 +388,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         const uint32_t pb = (uint32_t)t & 1u, nb1 = pb ^ 1u;
         const uint32_t st = (uint32_t)t, stn = st + 1u;
         bool busy = false;
+        TRACE_DECL
         if (active) {
             unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
             // issue the boundary polls first (all four words of each slot)
@@ -298,110 +403,191 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 }
 
             // deferred Phase 3 of cycle t-1
+            TRACE_EV(has_pend ? 1u : 0u);
             if (has_pend) { phase3(S, K, c, pend, t - 1, acc); has_pend = false; }
 
             // Phase 1
+            TRACE_P1_BEGIN
             if (MODE == 0u) phase1_ur(S, K, c, t);
-            else phase1_lspd(S, K, c, t);
+            else phase1_lspd_win(S, K, c, t, wbase, wmask);
+            TRACE_P1_END
 
-            // Phase 2: which input slots hold a flit this cycle.  All
-            // flits stay in shared memory (slot k<4: sflit, k=4: sinj).
-            uint32_t present = 0;
+            // Phase 2: latch.  Slots 0..3 = link inputs N,S,E,W
+            // (P:L199), slot 4 = the injection register.
+            uint32_t *const myfl = sfl + pb * np + i;
+            const uint32_t occ = *myfl;
+            *myfl = 0u;
+            uint32_t present = ((occ & 0x01010101u) * 0x01020408u) >> 24;   // byte d -> bit d
+            // All slots are read and every routing step below is computed for
+            // all five slots without branches (absent slots are masked): the
+            // five flits then form independent instruction chains the SM
+            // overlaps, instead of five divergent blocks executed in turn.
+            Flit f[5];
 #pragma unroll
-            for (uint32_t d = 0; d < 4; ++d)
-                if (((intl >> d) & 1u) && sst[(pb * 4u + d) * np + i] == st) present |= 1u << d;
-            // boundary inputs: spin on the LL stamps, then stage the flit
+            for (uint32_t d = 0; d < 4; ++d) {
+                const uint4 v = sflit[(pb * 4u + d) * np + i];
+                f[d] = Flit{v.x, v.y, v.z, v.w};
+            }
+            f[4] = Flit{0, 0, 0, 0};
+            // boundary inputs: poll all of this node's boundary slots together
+            // until each is complete for cycle t (word 0 carries stamp t and,
+            // for a flit rather than EMPTY, so do words 1..3)
             if (ext) {
+                uint32_t wait = ext, spins = 0;
+                while (true) {
 #pragma unroll
-                for (uint32_t d = 0; d < 4; ++d) {
-                    if (!((ext >> d) & 1u)) continue;
-                    const unsigned long long *slot = llp + inw[d];
-                    uint32_t spins = 0;
-                    unsigned long long w0 = xa[d], w1 = xb[d], w2 = xc[d], w3 = xd[d];
-                    // complete when word 0 carries this cycle's stamp and, for a
-                    // flit (not EMPTY), so do words 1..3
-                    while ((uint32_t)w0 != st ||
-                           ((uint32_t)(w0 >> 32) != LL_EMPTY &&
-                            ((uint32_t)w1 != st || (uint32_t)w2 != st || (uint32_t)w3 != st))) {
-                        if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
-                        const bool sys = (bedge >> d) & 1u;
-                        ll_load2(sys, slot, w0, w1);
-                        ll_load2(sys, slot + 2, w2, w3);
+                    for (uint32_t d = 0; d < 4; ++d) {
+                        if (!((wait >> d) & 1u)) continue;
+                        const uint32_t x = (uint32_t)(xa[d] >> 32);
+                        if ((uint32_t)xa[d] == st &&
+                            (x == LL_EMPTY || ((uint32_t)xb[d] == st && (uint32_t)xc[d] == st && (uint32_t)xd[d] == st))) {
+                            wait &= ~(1u << d);
+                            if (x != LL_EMPTY) {
+                                f[d] = Flit{x, (uint32_t)(xb[d] >> 32), (uint32_t)(xc[d] >> 32), (uint32_t)(xd[d] >> 32)};
+                                present |= 1u << d;
+                            }
+                        }
                     }
-                    const uint32_t x = (uint32_t)(w0 >> 32);
-                    if ((uint32_t)w0 == st && x != LL_EMPTY) {
-                        sflit[(pb * 4u + d) * np + i] =
-                            make_uint4(x, (uint32_t)(w1 >> 32), (uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32));
-                        present |= 1u << d;
-                    }
+                    if (!wait) break;
+                    if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
+#pragma unroll
+                    for (uint32_t d = 0; d < 4; ++d)
+                        if ((wait >> d) & 1u) {
+                            const bool sys = (bedge >> d) & 1u;
+                            ll_load2(sys, llp + inw[d], xa[d], xb[d]);
+                            ll_load2(sys, llp + inw[d] + 2, xc[d], xd[d]);
+                        }
                 }
             }
-            {
-                Flit fi;
-                if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, fi)) {
-                    sinj[i] = make_uint4(fi.x, fi.y, fi.z, fi.w);
-                    present |= 16u;
-                }
-            }
-            auto slot_flit = [&](uint32_t k) -> Flit {
-                const uint4 v = k < 4u ? sflit[(pb * 4u + k) * np + i] : sinj[i];
-                return Flit{v.x, v.y, v.z, v.w};
-            };
-            auto out = [&](uint32_t p, const Flit &f) {
-                const uint32_t slot = p ^ 1u;   // opp(p): N<->S (0,1), E<->W (2,3)
-                if ((ext >> p) & 1u) {
-                    const bool sys = (bedge >> p) & 1u;
-                    unsigned long long *o = ll_out(S, sys, p, nb1, pstride) + pick4(outw, p);
-                    ll_store2(sys, o + 2, llw(stn, f.z), llw(stn, f.w));
-                    ll_store2(sys, o, llw(stn, f.x), llw(stn, f.y));
-                } else {
-                    const uint32_t so = (nb1 * 4u + slot) * np + snb[p * np + i];
-                    sflit[so] = make_uint4(f.x, f.y, f.z, f.w);
-                    sst[so] = stn;
-                }
-            };
-            Flit ej;
+            TRACE_EXT_DONE
+            if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4])) present |= 16u;
+            TRACE_EV(((present & 16u) ? 32u : 0u) | (present ? 64u : 0u) | (ext ? 128u : 0u));
+
+            // first choices (eject at the destination, else x-port, else
+            // y-port: PMDR) and packed preferences: bit0 at the
+            // destination, bit1 has an x-port, [2:4) x-port, bit4 has a
+            // y-port, [5:7) y-port
+            uint32_t seen = 0, coll = 0, ports = 0, dm = 0, bad = 0;
+            uint64_t prefs = 0;
+            Flit ej = {0, 0, 0, 0};
             bool has_ej = false;
             uint32_t used = 0;
             if (present) {
-                // fast path over the present slots only: if the first choices
-                // are pairwise distinct, every flit takes its first choice
-                uint32_t seen = 0, fcs = 0;
-                bool coll = false;
-                for (uint32_t m = present; m; m &= m - 1u) {
-                    const uint32_t k = __ffs(m) - 1u;
-                    const uint32_t fc = first_choice(S, c, slot_flit(k), st, errf);
-                    coll |= (seen >> fc) & 1u;
-                    seen |= 1u << fc;
-                    fcs |= fc << (4u * k);
-                }
-                if (!coll) {
-                    for (uint32_t m = present; m; m &= m - 1u) {
-                        const uint32_t k = __ffs(m) - 1u, fc = (fcs >> (4u * k)) & 15u;
-                        const Flit f = slot_flit(k);
-                        if (fc == PX) { ej = f; has_ej = true; continue; }
-                        ++acc.hops;
-                        out(fc, f);
-                    }
-                    used = seen & 15u;
-                } else {
-                    // general case: full ranking + greedy
-                    Inputs in;
-                    in.present = present;
 #pragma unroll
-                    for (uint32_t k = 0; k < 5; ++k)
-                        if ((present >> k) & 1u) in.f[k] = slot_flit(k);
-                    used = route_select(S, c, in, t, acc, ej, has_ej, out);
+                for (uint32_t k = 0; k < 5; ++k) {
+                    const uint32_t pk = (present >> k) & 1u;
+                    bad |= pk & (st - f[k].z > LIFE_MAX ? 1u : 0u);   // R32
+                    const uint32_t dst = f_dst(f[k]);
+                    const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
+                    const uint32_t xp = dx > c.x ? PE : PW, yp = dy > c.y ? PS : PN;
+                    const uint32_t pw = dst == c.n ? 1u
+                                                   : ((dx != c.x ? 2u | (xp << 2) : 0u) |
+                                                      (dy != c.y ? 16u | (yp << 5) : 0u));
+                    const uint32_t fc = dst == c.n ? PX : (dx != c.x ? xp : yp);
+                    prefs |= (uint64_t)pw << (8u * k);
+                    const uint32_t b = pk << fc;
+                    coll |= seen & b;
+                    seen |= b;
+                    ports |= fc << (4u * k);
+                }
+                if (bad) errf |= ERR_AGE;
+                used = seen & 15u;
+                TRACE_EV(coll ? 16u : 0u);
+                if (coll) {
+                    // two flits want the same port: rank them ("Priority Sort",
+                    // P:L129; R1, R2) and let each take, in rank order, the
+                    // eject link if at its destination and still free, else
+                    // its first free productive port, else the first free
+                    // existing port in N,S,E,W with age+1 (R3-R6).
+                    // The injected flit (age 0, lifetime 0) ranks last.
+                    uint64_t key[4];
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) {
+                        const uint32_t life = st - f[k].z;   // overflow flagged above (R32)
+                        key[k] = ((uint64_t)(life > LIFE_MAX ? LIFE_MAX : life) << 21) | (NODE_MASK - f_src(f[k]));
+                        if (S.prio == 0u) key[k] |= (uint64_t)f_age(f[k]) << 48;
+                        if (!((present >> k) & 1u)) key[k] = 0ull;
+                    }
+                    uint32_t rk[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (uint32_t a = 0; a < 4; ++a)
+#pragma unroll
+                        for (uint32_t b = a + 1; b < 4; ++b) {
+                            if (key[a] > key[b]) ++rk[b];
+                            else ++rk[a];
+                        }
+                    uint32_t ord = 4u << 16;
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) ord |= k << (4u * rk[k]);
+                    used = 0;
+                    ports = 0;
+                    bool ejd = false;
+#pragma unroll
+                    for (uint32_t r = 0; r < 5; ++r) {
+                        const uint32_t k = (ord >> (4u * r)) & 15u;
+                        if (!((present >> k) & 1u)) continue;
+                        const uint32_t pw = (uint32_t)(prefs >> (8u * k)) & 0xFFu;
+                        const uint32_t xp = (pw >> 2) & 3u, yp = (pw >> 5) & 3u;
+                        uint32_t p;
+                        if ((pw & 1u) && !ejd) {
+                            ejd = true;
+                            p = PX;
+                        } else {
+                            if ((pw & 2u) && !((used >> xp) & 1u)) p = xp;
+                            else if ((pw & 16u) && !((used >> yp) & 1u)) p = yp;
+                            else { p = __ffs(exist & ~used) - 1u; dm |= 1u << k; }
+                            used |= 1u << p;
+                        }
+                        ports |= p << (4u * k);
+                    }
                 }
             }
-            // boundary ports without a flit carry an explicit EMPTY every cycle
-            const uint32_t idle_ext = ext & ~used;
+            // Outputs across the tile boundary first: they are on the critical
+            // path of the neighbouring tiles.  Routed flits, then an explicit
+            // EMPTY on every other boundary port (every cycle).
+            if (ext) {
+                if (present) {
 #pragma unroll
-            for (uint32_t p = 0; p < 4; ++p)
-                if ((idle_ext >> p) & 1u) {
-                    const bool sys = (bedge >> p) & 1u;
-                    ll_store1(sys, ll_out(S, sys, p, nb1, pstride) + outw[p], llw(stn, LL_EMPTY));
+                    for (uint32_t k = 0; k < 5; ++k) {
+                        const uint32_t p = (ports >> (4u * k)) & 15u;
+                        if (!((present >> k) & 1u) || p >= 4u || !((ext >> p) & 1u)) continue;
+                        Flit g = f[k];
+                        if ((dm >> k) & 1u) f_set_age(g, min(f_age(g) + 1u, AGE_MAX));
+                        const bool sys = (bedge >> p) & 1u;
+                        unsigned long long *o = ll_out(S, sys, p, nb1, pstride) + pick4(outw, p);
+                        ll_store2(sys, o + 2, llw(stn, g.z), llw(stn, g.w));
+                        ll_store2(sys, o, llw(stn, g.x), llw(stn, g.y));
+                    }
                 }
+                const uint32_t idle_ext = ext & ~used;
+#pragma unroll
+                for (uint32_t p = 0; p < 4; ++p)
+                    if ((idle_ext >> p) & 1u) {
+                        const bool sys = (bedge >> p) & 1u;
+                        ll_store1(sys, ll_out(S, sys, p, nb1, pstride) + outw[p], llw(stn, LL_EMPTY));
+                    }
+            }
+            // then the ejected flit (<= 1) and the flits that stay in the tile
+            // (predicated shared-memory stores); counters for all
+            if (present) {
+#pragma unroll
+                for (uint32_t k = 0; k < 5; ++k) {
+                    const uint32_t p = (ports >> (4u * k)) & 15u;
+                    const bool pk = (present >> k) & 1u;
+                    if (pk && p == PX) { ej = f[k]; has_ej = true; }
+                    const bool go = pk && p < 4u;
+                    const uint32_t dk = (dm >> k) & 1u;             // P:L116 age increment
+                    uint32_t a = f_age(f[k]) + dk;
+                    if (a > AGE_MAX) { errf |= ERR_AGE; a = AGE_MAX; }
+                    f_set_age(f[k], a);
+                    acc.defl += dk;
+                    acc.hops += go ? 1u : 0u;
+                    const uint32_t nb = ((p < 2u ? nbr01 : nbr23) >> (16u * (p & 1u))) & 0xFFFFu;
+                    const bool gi = go && !((ext >> p) & 1u);
+                    sts128_if(gi, sflit + (nb1 * 4u + (p ^ 1u)) * np + nb, f[k]);
+                    sts8_if(gi, reinterpret_cast<uint8_t *>(sfl + nb1 * np + nb) + (p ^ 1u));   // opp(p)
+                }
+            }
             if (has_ej) {
                 // while draining, quiescence is judged at the end of each cycle,
                 // so the service is not deferred there
@@ -409,9 +595,22 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 else { pend = ej; has_pend = true; if (MODE == 1u) prefetch_service(S, c, ej); }
             }
             if (DRAIN) busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
-            // the generation draw of cycle t+1, off the critical path
-            predraw(S, c, t + 1);
         }
+        if (windows) {
+            // windows for cycle t+1: idle cores, cores whose wait expires at
+            // t+1, and the deferred service of a reply flit (may complete the
+            // access); also prefetch the set a memory fill installs into
+            bool need = false;
+            if (active) {
+                const uint32_t t1 = stn, mode = core_mode(c.hot);
+                const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ t1) & 0x1FFFFFFFu) == 0u);
+                if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
+                need = (mode == MIDLE || expiring || (has_pend && f_kind(pend) == KRA)) && t1 - wbase >= 32u;
+            }
+            TRACE_EV(__any_sync(FULL, need) ? 8u : 0u);
+            refresh(need, t + 1);
+        }
+        TRACE_END
         // The cycle barrier is a full BAR.SYNC: it orders this cycle's shared-
         // memory link stores before the next cycle's loads (a reducing barrier,
         // __syncthreads_or, measurably did not on sm_100a).
@@ -433,12 +632,12 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         }
         const uint32_t be = (uint32_t)tend & 1u;
         const uint8_t ste = stamp_of(tend);
+        const uint32_t occ = sfl[be * np + i];
         uint32_t gfl = 0;
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
-            const uint32_t si = (be * 4u + d) * np + i;
-            if (((intl >> d) & 1u) && sst[si] == (uint32_t)tend) {
-                S.flit[be][(size_t)d * S.nloc + c.l] = sflit[si];
+            if (((intl >> d) & 1u) && ((occ >> (8u * d)) & 0xFFu)) {
+                S.flit[be][(size_t)d * S.nloc + c.l] = sflit[(be * 4u + d) * np + i];
                 gfl |= (uint32_t)ste << (8u * d);
             }
         }
@@ -498,7 +697,7 @@ __global__ void k_ll_reset(Dev S, uint64_t t)
 // ------------------------------------------------------------------ host side
 size_t tiled_smem_bytes(const Dev &S, uint32_t np, bool with_hist)
 {
-    return (size_t)np * (9u * 16u + 12u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
+    return (size_t)np * (8u * 16u + 2u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
 }
 
 // Pick TX x TY tiles for one band (<= tiles_budget CTAs, <= TILE_BLOCK_MAX

@@ -15,7 +15,8 @@ ap.add_argument("--cycles", type=int, default=200)
 ap.add_argument("--launches", type=int, default=3)
 ap.add_argument("--engine", type=int, default=0)
 a = ap.parse_args()
-cfg = {"c3": W.c3, "c2": W.c2, "c5": W.c5, "c4ur": lambda: W.c4(0.3)}[a.workload]()
+cfg = {"c3": W.c3, "c2": W.c2, "c5": W.c5, "c4ur": lambda: W.c4(0.3),
+       "ur0": lambda: W.make(mesh_w=208, mesh_h=208, mode=W.MODE_UR, thr_inj=0)}[a.workload]()
 s = pkg.NocSim(cfg, engine=a.engine)
 s.run(a.warm)
 for _ in range(a.launches):
