@@ -323,7 +323,7 @@ __device__ __forceinline__ void phase1_ur(const Dev &S, const Sink &K, NodeCtx &
     bool fire = false;
     if (S.has_script && script_next(S, c, t, v)) {
         fire = true; dst = v;
-    } else {
+    } else if (S.thr_inj != 0u) {    // at rate 0 no draw can fire (r0 < 0 never holds)
         fire = draw_now(S, c, t, dst);
     }
     if (fire) {

@@ -338,8 +338,10 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     s->engine = cfg->engine;
     if (s->P > 1 && s->engine != NOC_ENGINE_AUTO && s->engine != NOC_ENGINE_TILED && s->engine != NOC_ENGINE_TILED4)
         return bail(fail(NOC_EINVAL, "row bands need a TILED engine"));
-    // AUTO tries TILED4 (4 lanes per node, 2 CTAs per SM), then TILED, then PERSIST
-    for (uint32_t cand : {NOC_ENGINE_TILED4, NOC_ENGINE_TILED}) {
+    // AUTO tries TILED (one thread per node), then TILED4 (4 lanes per node,
+    // 2 CTAs per SM), then PERSIST: TILED is the fastest at the bench size
+    // (DESIGN 6.4, profiles/r01_ab_engines.txt)
+    for (uint32_t cand : {NOC_ENGINE_TILED, NOC_ENGINE_TILED4}) {
         if (!(s->engine == NOC_ENGINE_AUTO || s->engine == cand)) continue;
         const bool four = cand == NOC_ENGINE_TILED4;
         bool ok = true;
@@ -409,7 +411,11 @@ static int check_err(noc_sim *s)
     CU(cudaStreamSynchronize(s->stream));
     if (err) {
         s->poisoned = 1;
-        if (err & 0x80000000u) return fail(NOC_ECUDA, "boundary / neighbour wait timed out");
+        if (err & 0x80000000u) {
+            char b[96];
+            snprintf(b, sizeof b, "boundary / neighbour wait timed out (flags 0x%08x)", err);
+            return fail(NOC_ECUDA, b);
+        }
         if (err & (ERR_AGE | ERR_PEND)) return fail(NOC_EOVERFLOW, "field width exceeded (flit age, lifetime or pend)");
         return fail(NOC_ECUDA, "model assertion failed on device (protocol / EV holder)");
     }

@@ -22,6 +22,7 @@
 // The per-node model code is node_logic.cuh's (bit-identical to every engine).
 #include "node_logic.cuh"
 #include "kernels.h"
+#include <cstdio>
 
 namespace noc {
 
@@ -59,20 +60,6 @@ __device__ __forceinline__ void st_relaxed_x2(unsigned long long *p, unsigned lo
 __device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t p)
 {
     return p == 0u ? a[0] : p == 1u ? a[1] : p == 2u ? a[2] : a[3];
-}
-
-// Predicated shared-memory stores (no branch around them)
-__device__ __forceinline__ void sts128_if(bool c, uint4 *p, const Flit &v)
-{
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n\t}"
-                 ::"r"((uint32_t)c), "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-__device__ __forceinline__ void sts8_if(bool c, uint8_t *p)
-{
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u8 [%1], %2;\n\t}"
-                 ::"r"((uint32_t)c), "r"(a), "r"(1u) : "memory");
 }
 
 struct TileShape {
@@ -232,6 +219,54 @@ extern "C" int noc_trace_ctl(int on, void *host, size_t bytes)
 #define TRACE_END
 #endif
 
+// Shared-memory access by 32-bit shared-window address (no generic->shared
+// conversion in the loop); the stores are predicated, not branched around.
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts32_if(bool c, uint32_t a, uint32_t v)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u32 [%1], %2;\n\t}"
+                 ::"r"((uint32_t)c), "r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void lds128_if(bool c, uint32_t a, Flit &f)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
+                 : "+r"(f.x), "+r"(f.y), "+r"(f.z), "+r"(f.w) : "r"((uint32_t)c), "r"(a) : "memory");
+}
+__device__ __forceinline__ void sts128_if(bool c, uint32_t a, const Flit &v)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n\t}"
+                 ::"r"((uint32_t)c), "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void sts8_if(bool c, uint32_t a)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u8 [%1], %2;\n\t}"
+                 ::"r"((uint32_t)c), "r"(a), "r"(1u) : "memory");
+}
+
+// f[k] for a runtime k in [0, 5) without indexing a local array
+__device__ __forceinline__ Flit pick5(const Flit (&f)[5], uint32_t k)
+{
+    Flit r = f[4];
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j)
+        if (k == j) r = f[j];
+    return r;
+}
+
+// One cross-tile input port of a boundary node: where its LL words are read.
+struct ExtIn {
+    uint32_t port;   // N, S, E or W; NOPORT if none
+    uint32_t inw;    // LL word index (parity 0) of this node's input slot
+    uint32_t outw;   // LL word index (parity 0) of the receiver's slot for output `port`
+    bool sys;        // crosses the band edge (system scope)
+};
+constexpr uint32_t NOPORT = 8u;
+
 template <uint32_t MODE, bool DRAIN>
 __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
@@ -260,6 +295,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         for (uint32_t k = i; k < nsm; k += blockDim.x) scnt[k] = 0u;
         if (i == 0) { s_abort = 0; s_busy[0] = s_busy[1] = 0u; }
     }
+    // shared-window addresses: flit slot d of node slot j at parity b is
+    // fa + b*FSTR + (d*np + j)*16; its occupancy byte oa + b*OSTR + j*4 + d
+    const uint32_t fa = (uint32_t)__cvta_generic_to_shared(sflit);
+    const uint32_t oa = (uint32_t)__cvta_generic_to_shared(sfl);
+    const uint32_t FSTR = 64u * np, OSTR = 4u * np;
 
     // ---- node registers (persist for the whole launch)
     NodeCtx c;
@@ -283,9 +323,9 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     uint32_t exist = 0;    // bit d: port d has a neighbour
     uint32_t ext = 0;      // bit d: port d crosses the tile boundary
     uint32_t intl = 0;     // bit d: port d exists inside the tile
-    uint32_t bedge = 0;    // bit d: port d crosses the band edge (N: 0, S: 1)
-    uint32_t inw[4] = {0, 0, 0, 0}, outw[4] = {0, 0, 0, 0};
-    uint32_t nbr01 = 0, nbr23 = 0;   // neighbour node slot of ports N,S / E,W (16 bits each)
+    uint32_t na[4] = {0, 0, 0, 0};   // internal port p: neighbour's flit slot offset | occupancy byte offset << 16
+    ExtIn ex[4] = {{NOPORT, 0, 0, false}, {NOPORT, 0, 0, false}, {NOPORT, 0, 0, false}, {NOPORT, 0, 0, false}};
+    uint32_t nex = 0;
     c.deg = 0;
     const uint32_t b0 = (uint32_t)t0 & 1u;
     if (active) {
@@ -300,7 +340,8 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                (lx == 0 ? 8u : 0u)) & exist;
         intl = exist & ~ext;
         c.deg = __popc(exist);
-        bedge = ((c.y == S.row0 && c.y > 0) ? 1u : 0u) | ((c.y + 1 == S.row0 + S.rows && c.y + 1 < S.H) ? 2u : 0u);
+        const uint32_t bedge =
+            ((c.y == S.row0 && c.y > 0) ? 1u : 0u) | ((c.y + 1 == S.row0 + S.rows && c.y + 1 < S.H) ? 2u : 0u);
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
             uint32_t m = c.l, mi = 0;
@@ -310,19 +351,25 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             case PE: m = c.l + 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx + 1, lyy); break;
             default: m = c.l - 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx - 1, lyy); break;
             }
+            if ((intl >> d) & 1u) na[d] = (((d ^ 1u) * np + mi) * 16u) | ((mi * 4u + (d ^ 1u)) << 16);
             if ((ext >> d) & 1u) {
-                inw[d] = (uint32_t)ll_index(S, 0, d, c.l, 0);
-                if ((bedge >> d) & 1u) {
+                ExtIn e;
+                e.port = d;
+                e.inw = (uint32_t)ll_index(S, 0, d, c.l, 0);
+                e.sys = (bedge >> d) & 1u;
+                if (e.sys) {
                     // the receiver is in the neighbour band: its local index there
                     const uint32_t nr = S.nloc_nb[d];
                     const uint32_t lr = d == PN ? c.l - S.W + nr : c.l + S.W - S.nloc;
-                    outw[d] = (uint32_t)(((size_t)(d ^ 1u) * nr + lr) * 4u);
+                    e.outw = (uint32_t)(((size_t)(d ^ 1u) * nr + lr) * 4u);
                 } else {
-                    outw[d] = (uint32_t)ll_index(S, 0, d ^ 1u, m, 0);
+                    e.outw = (uint32_t)ll_index(S, 0, d ^ 1u, m, 0);
                 }
+#pragma unroll
+                for (uint32_t j = 0; j < 4; ++j)
+                    if (j == nex) ex[j] = e;
+                ++nex;
             }
-            if (d < 2u) nbr01 |= mi << (16u * d);
-            else nbr23 |= mi << (16u * (d - 2u));
         }
         // internal inputs of cycle t0 (spilled by the previous launch)
         const uint32_t fl = S.flag[b0][c.l];
@@ -382,6 +429,8 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     Acc acc = {0, 0, 0, 0};
     Flit pend = {0, 0, 0, 0};
     bool has_pend = false;
+    const uint32_t own_f = fa + i * 16u, own_o = oa + i * 4u;
+    const ExtIn &e0 = ex[0], &e1 = ex[1];
 
     for (uint32_t cc = 0; cc < ncyc; ++cc) {
         const uint64_t t = t0 + cc;
@@ -390,209 +439,233 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         bool busy = false;
         TRACE_DECL
         if (active) {
-            unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
-            // issue the boundary polls first (all four words of each slot)
-            unsigned long long xa[4] = {0, 0, 0, 0}, xb[4] = {0, 0, 0, 0}, xc[4] = {0, 0, 0, 0},
-                               xd[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (uint32_t d = 0; d < 4; ++d)
-                if ((ext >> d) & 1u) {
-                    const bool sys = (bedge >> d) & 1u;
-                    ll_load2(sys, llp + inw[d], xa[d], xb[d]);
-                    ll_load2(sys, llp + inw[d] + 2, xc[d], xd[d]);
+            const unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
+            // (0) issue the boundary polls first (all four words of each slot)
+            unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0w = 0, b1w = 0, b2w = 0, b3w = 0;
+            if (ext) {
+                ll_load2(e0.sys, llp + e0.inw, a0, a1);
+                ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
+                if (e1.port != NOPORT) {
+                    ll_load2(e1.sys, llp + e1.inw, b0w, b1w);
+                    ll_load2(e1.sys, llp + e1.inw + 2, b2w, b3w);
                 }
+            }
 
-            // deferred Phase 3 of cycle t-1
+            // (1) deferred Phase 3 of cycle t-1, then Phase 1
             TRACE_EV(has_pend ? 1u : 0u);
             if (has_pend) { phase3(S, K, c, pend, t - 1, acc); has_pend = false; }
-
-            // Phase 1
             TRACE_P1_BEGIN
             if (MODE == 0u) phase1_ur(S, K, c, t);
             else phase1_lspd_win(S, K, c, t, wbase, wmask);
             TRACE_P1_END
 
-            // Phase 2: latch.  Slots 0..3 = link inputs N,S,E,W
-            // (P:L199), slot 4 = the injection register.
-            uint32_t *const myfl = sfl + pb * np + i;
-            const uint32_t occ = *myfl;
-            *myfl = 0u;
+            // (2) latch.  Slots 0..3 = link inputs N,S,E,W,
+            // slot 4 = the injection register.  The occupancy word
+            // is consumed (cleared) here.
+            const uint32_t ow = own_o + pb * OSTR;
+            const uint32_t occ = lds32(ow);
+            sts32_if(occ != 0u, ow, 0u);
             uint32_t present = ((occ & 0x01010101u) * 0x01020408u) >> 24;   // byte d -> bit d
-            // All slots are read and every routing step below is computed for
-            // all five slots without branches (absent slots are masked): the
-            // five flits then form independent instruction chains the SM
-            // overlaps, instead of five divergent blocks executed in turn.
-            Flit f[5];
-#pragma unroll
-            for (uint32_t d = 0; d < 4; ++d) {
-                const uint4 v = sflit[(pb * 4u + d) * np + i];
-                f[d] = Flit{v.x, v.y, v.z, v.w};
-            }
-            f[4] = Flit{0, 0, 0, 0};
-            // boundary inputs: poll all of this node's boundary slots together
-            // until each is complete for cycle t (word 0 carries stamp t and,
-            // for a flit rather than EMPTY, so do words 1..3)
+            const uint32_t fw = own_f + pb * FSTR;
+            // boundary inputs: poll until each cross-tile slot is complete for
+            // cycle t (word 0 carries stamp t and, for a flit rather than
+            // EMPTY, so do words 1..3); a flit is parked in the node's own
+            // shared slot so all four link inputs are latched alike below
             if (ext) {
-                uint32_t wait = ext, spins = 0;
+                bool w0 = true, w1 = e1.port != NOPORT, w2 = ex[2].port != NOPORT, w3 = ex[3].port != NOPORT;
+                uint32_t spins = 0;
                 while (true) {
 #pragma unroll
-                    for (uint32_t d = 0; d < 4; ++d) {
-                        if (!((wait >> d) & 1u)) continue;
-                        const uint32_t x = (uint32_t)(xa[d] >> 32);
-                        if ((uint32_t)xa[d] == st &&
-                            (x == LL_EMPTY || ((uint32_t)xb[d] == st && (uint32_t)xc[d] == st && (uint32_t)xd[d] == st))) {
-                            wait &= ~(1u << d);
-                            if (x != LL_EMPTY) {
-                                f[d] = Flit{x, (uint32_t)(xb[d] >> 32), (uint32_t)(xc[d] >> 32), (uint32_t)(xd[d] >> 32)};
-                                present |= 1u << d;
-                            }
+                    for (uint32_t j = 2; j < 4; ++j) {
+                        bool &wj = j == 2 ? w2 : w3;
+                        if (!wj) continue;
+                        unsigned long long c0, c1, c2, c3;
+                        ll_load2(ex[j].sys, llp + ex[j].inw, c0, c1);
+                        ll_load2(ex[j].sys, llp + ex[j].inw + 2, c2, c3);
+                        if ((uint32_t)c0 != st) continue;
+                        const uint32_t x = (uint32_t)(c0 >> 32);
+                        if (x == LL_EMPTY) wj = false;
+                        else if ((uint32_t)c1 == st && (uint32_t)c2 == st && (uint32_t)c3 == st) {
+                            wj = false;
+                            sts128_if(true, fw + ex[j].port * 16u * np,
+                                      Flit{x, (uint32_t)(c1 >> 32), (uint32_t)(c2 >> 32), (uint32_t)(c3 >> 32)});
+                            present |= 1u << ex[j].port;
                         }
                     }
-                    if (!wait) break;
-                    if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
-#pragma unroll
-                    for (uint32_t d = 0; d < 4; ++d)
-                        if ((wait >> d) & 1u) {
-                            const bool sys = (bedge >> d) & 1u;
-                            ll_load2(sys, llp + inw[d], xa[d], xb[d]);
-                            ll_load2(sys, llp + inw[d] + 2, xc[d], xd[d]);
+                    if (w0 && (uint32_t)a0 == st) {
+                        const uint32_t x = (uint32_t)(a0 >> 32);
+                        if (x == LL_EMPTY) w0 = false;
+                        else if ((uint32_t)a1 == st && (uint32_t)a2 == st && (uint32_t)a3 == st) {
+                            w0 = false;
+                            sts128_if(true, fw + e0.port * 16u * np,
+                                      Flit{x, (uint32_t)(a1 >> 32), (uint32_t)(a2 >> 32), (uint32_t)(a3 >> 32)});
+                            present |= 1u << e0.port;
                         }
+                    }
+                    if (w1 && (uint32_t)b0w == st) {
+                        const uint32_t x = (uint32_t)(b0w >> 32);
+                        if (x == LL_EMPTY) w1 = false;
+                        else if ((uint32_t)b1w == st && (uint32_t)b2w == st && (uint32_t)b3w == st) {
+                            w1 = false;
+                            sts128_if(true, fw + e1.port * 16u * np,
+                                      Flit{x, (uint32_t)(b1w >> 32), (uint32_t)(b2w >> 32), (uint32_t)(b3w >> 32)});
+                            present |= 1u << e1.port;
+                        }
+                    }
+                    if (!(w0 || w1 || w2 || w3)) break;
+                    if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
+                    if (w0) {
+                        ll_load2(e0.sys, llp + e0.inw, a0, a1);
+                        ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
+                    }
+                    if (w1) {
+                        ll_load2(e1.sys, llp + e1.inw, b0w, b1w);
+                        ll_load2(e1.sys, llp + e1.inw + 2, b2w, b3w);
+                    }
                 }
             }
             TRACE_EXT_DONE
+            Flit f[5];
+#pragma unroll
+            for (uint32_t d = 0; d < 5; ++d) f[d] = Flit{0, 0, 0, 0};
+#pragma unroll
+            for (uint32_t d = 0; d < 4; ++d) lds128_if((present >> d) & 1u, fw + d * 16u * np, f[d]);
             if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4])) present |= 16u;
             TRACE_EV(((present & 16u) ? 32u : 0u) | (present ? 64u : 0u) | (ext ? 128u : 0u));
 
-            // first choices (eject at the destination, else x-port, else
-            // y-port: PMDR) and packed preferences: bit0 at the
-            // destination, bit1 has an x-port, [2:4) x-port, bit4 has a
-            // y-port, [5:7) y-port
-            uint32_t seen = 0, coll = 0, ports = 0, dm = 0, bad = 0;
-            uint64_t prefs = 0;
-            Flit ej = {0, 0, 0, 0};
-            bool has_ej = false;
-            uint32_t used = 0;
-            if (present) {
+            // (3) first choices (eject at the destination, else x-port, else
+            // y-port: PMDR).  If they are pairwise distinct every flit
+            // takes its first choice whatever the ranking.  port[k] in
+            // `ports` nibble k; inv nibble p = the slot routed to port p
+            // (p = 4: the ejected flit)
+            uint32_t seen = 0, coll = 0, ports = 0, inv = 0, bad = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < 5; ++k) {
+                const uint32_t pk = (present >> k) & 1u;
+                bad |= pk & (st - f[k].z > LIFE_MAX ? 1u : 0u);   // R32
+                const uint32_t dst = f_dst(f[k]);
+                const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
+                const uint32_t fc = dst == c.n ? PX : dx != c.x ? (dx > c.x ? PE : PW) : (dy > c.y ? PS : PN);
+                const uint32_t b = pk << fc;
+                coll |= seen & b;
+                seen |= b;
+                ports |= fc << (4u * k);
+                inv |= pk ? k << (4u * fc) : 0u;
+            }
+            if (bad) errf |= ERR_AGE;
+            uint32_t used = seen & 15u;
+            bool has_ej = (seen >> PX) & 1u;
+            TRACE_EV(coll ? 16u : 0u);
+            if (coll) {
+                // two flits want the same port: rank them ("Priority Sort",
+                // P:L129; R1, R2) and let each take, in rank order, the eject
+                // link if at its destination and still free, else its first
+                // free productive port, else the first free existing port in
+                // N,S,E,W with age+1 (R3-R6).
+                // The injected flit (age 0, lifetime 0) always ranks last.
+                uint64_t key[4];
+                uint64_t prefs = 0;
 #pragma unroll
                 for (uint32_t k = 0; k < 5; ++k) {
-                    const uint32_t pk = (present >> k) & 1u;
-                    bad |= pk & (st - f[k].z > LIFE_MAX ? 1u : 0u);   // R32
                     const uint32_t dst = f_dst(f[k]);
                     const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
                     const uint32_t xp = dx > c.x ? PE : PW, yp = dy > c.y ? PS : PN;
                     const uint32_t pw = dst == c.n ? 1u
                                                    : ((dx != c.x ? 2u | (xp << 2) : 0u) |
                                                       (dy != c.y ? 16u | (yp << 5) : 0u));
-                    const uint32_t fc = dst == c.n ? PX : (dx != c.x ? xp : yp);
                     prefs |= (uint64_t)pw << (8u * k);
-                    const uint32_t b = pk << fc;
-                    coll |= seen & b;
-                    seen |= b;
-                    ports |= fc << (4u * k);
-                }
-                if (bad) errf |= ERR_AGE;
-                used = seen & 15u;
-                TRACE_EV(coll ? 16u : 0u);
-                if (coll) {
-                    // two flits want the same port: rank them ("Priority Sort",
-                    // P:L129; R1, R2) and let each take, in rank order, the
-                    // eject link if at its destination and still free, else
-                    // its first free productive port, else the first free
-                    // existing port in N,S,E,W with age+1 (R3-R6).
-                    // The injected flit (age 0, lifetime 0) ranks last.
-                    uint64_t key[4];
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) {
-                        const uint32_t life = st - f[k].z;   // overflow flagged above (R32)
+                    if (k < 4) {
+                        const uint32_t life = st - f[k].z;
                         key[k] = ((uint64_t)(life > LIFE_MAX ? LIFE_MAX : life) << 21) | (NODE_MASK - f_src(f[k]));
                         if (S.prio == 0u) key[k] |= (uint64_t)f_age(f[k]) << 48;
                         if (!((present >> k) & 1u)) key[k] = 0ull;
                     }
-                    uint32_t rk[4] = {0, 0, 0, 0};
-#pragma unroll
-                    for (uint32_t a = 0; a < 4; ++a)
-#pragma unroll
-                        for (uint32_t b = a + 1; b < 4; ++b) {
-                            if (key[a] > key[b]) ++rk[b];
-                            else ++rk[a];
-                        }
-                    uint32_t ord = 4u << 16;
-#pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) ord |= k << (4u * rk[k]);
-                    used = 0;
-                    ports = 0;
-                    bool ejd = false;
-#pragma unroll
-                    for (uint32_t r = 0; r < 5; ++r) {
-                        const uint32_t k = (ord >> (4u * r)) & 15u;
-                        if (!((present >> k) & 1u)) continue;
-                        const uint32_t pw = (uint32_t)(prefs >> (8u * k)) & 0xFFu;
-                        const uint32_t xp = (pw >> 2) & 3u, yp = (pw >> 5) & 3u;
-                        uint32_t p;
-                        if ((pw & 1u) && !ejd) {
-                            ejd = true;
-                            p = PX;
-                        } else {
-                            if ((pw & 2u) && !((used >> xp) & 1u)) p = xp;
-                            else if ((pw & 16u) && !((used >> yp) & 1u)) p = yp;
-                            else { p = __ffs(exist & ~used) - 1u; dm |= 1u << k; }
-                            used |= 1u << p;
-                        }
-                        ports |= p << (4u * k);
-                    }
                 }
+                uint32_t rk[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (uint32_t a = 0; a < 4; ++a)
+#pragma unroll
+                    for (uint32_t b = a + 1; b < 4; ++b) {
+                        if (key[a] > key[b]) ++rk[b];
+                        else ++rk[a];
+                    }
+                uint32_t ord = 4u << 16;
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) ord |= k << (4u * rk[k]);
+                used = 0;
+                ports = 0;
+                inv = 0;
+                has_ej = false;
+                uint32_t dm = 0;
+#pragma unroll
+                for (uint32_t r = 0; r < 5; ++r) {
+                    const uint32_t k = (ord >> (4u * r)) & 15u;
+                    if (!((present >> k) & 1u)) continue;
+                    const uint32_t pw = (uint32_t)(prefs >> (8u * k)) & 0xFFu;
+                    const uint32_t xp = (pw >> 2) & 3u, yp = (pw >> 5) & 3u;
+                    uint32_t p;
+                    if ((pw & 1u) && !has_ej) {
+                        has_ej = true;
+                        p = PX;
+                    } else {
+                        if ((pw & 2u) && !((used >> xp) & 1u)) p = xp;
+                        else if ((pw & 16u) && !((used >> yp) & 1u)) p = yp;
+                        else { p = __ffs(exist & ~used) - 1u; dm |= 1u << k; }
+                        used |= 1u << p;
+                    }
+                    ports |= p << (4u * k);
+                    inv |= k << (4u * p);
+                }
+                // P:L116 age increment of the deflected flits
+#pragma unroll
+                for (uint32_t k = 0; k < 5; ++k) {
+                    if (!((dm >> k) & 1u)) continue;
+                    uint32_t a = f_age(f[k]) + 1u;
+                    if (a > AGE_MAX) { errf |= ERR_AGE; a = AGE_MAX; }
+                    f_set_age(f[k], a);
+                }
+                acc.defl += __popc(dm);
             }
-            // Outputs across the tile boundary first: they are on the critical
-            // path of the neighbouring tiles.  Routed flits, then an explicit
-            // EMPTY on every other boundary port (every cycle).
+            acc.hops += __popc(used);
+            // (4) outputs across the tile boundary first: they are on the
+            // critical path of the neighbouring tiles.  A routed flit, else an
+            // explicit EMPTY, on every boundary port every cycle.
             if (ext) {
-                if (present) {
 #pragma unroll
-                    for (uint32_t k = 0; k < 5; ++k) {
-                        const uint32_t p = (ports >> (4u * k)) & 15u;
-                        if (!((present >> k) & 1u) || p >= 4u || !((ext >> p) & 1u)) continue;
-                        Flit g = f[k];
-                        if ((dm >> k) & 1u) f_set_age(g, min(f_age(g) + 1u, AGE_MAX));
-                        const bool sys = (bedge >> p) & 1u;
-                        unsigned long long *o = ll_out(S, sys, p, nb1, pstride) + pick4(outw, p);
-                        ll_store2(sys, o + 2, llw(stn, g.z), llw(stn, g.w));
-                        ll_store2(sys, o, llw(stn, g.x), llw(stn, g.y));
+                for (uint32_t j = 0; j < 4; ++j) {
+                    const ExtIn &e = ex[j];
+                    if (e.port == NOPORT) continue;
+                    unsigned long long *o = ll_out(S, e.sys, e.port, nb1, pstride) + e.outw;
+                    if ((used >> e.port) & 1u) {
+                        const Flit g = pick5(f, (inv >> (4u * e.port)) & 15u);
+                        ll_store2(e.sys, o + 2, llw(stn, g.z), llw(stn, g.w));
+                        ll_store2(e.sys, o, llw(stn, g.x), llw(stn, g.y));
+                    } else {
+                        ll_store1(e.sys, o, llw(stn, LL_EMPTY));
                     }
                 }
-                const uint32_t idle_ext = ext & ~used;
-#pragma unroll
-                for (uint32_t p = 0; p < 4; ++p)
-                    if ((idle_ext >> p) & 1u) {
-                        const bool sys = (bedge >> p) & 1u;
-                        ll_store1(sys, ll_out(S, sys, p, nb1, pstride) + outw[p], llw(stn, LL_EMPTY));
-                    }
             }
-            // then the ejected flit (<= 1) and the flits that stay in the tile
-            // (predicated shared-memory stores); counters for all
-            if (present) {
+            // (5) flits that stay in the tile: predicated shared-memory stores
+            // into the neighbour's slot opp(p) of cycle t+1
+            if (used & intl) {
+                const uint32_t nf = fa + nb1 * FSTR, no = oa + nb1 * OSTR;
 #pragma unroll
                 for (uint32_t k = 0; k < 5; ++k) {
                     const uint32_t p = (ports >> (4u * k)) & 15u;
-                    const bool pk = (present >> k) & 1u;
-                    if (pk && p == PX) { ej = f[k]; has_ej = true; }
-                    const bool go = pk && p < 4u;
-                    const uint32_t dk = (dm >> k) & 1u;             // P:L116 age increment
-                    uint32_t a = f_age(f[k]) + dk;
-                    if (a > AGE_MAX) { errf |= ERR_AGE; a = AGE_MAX; }
-                    f_set_age(f[k], a);
-                    acc.defl += dk;
-                    acc.hops += go ? 1u : 0u;
-                    const uint32_t nb = ((p < 2u ? nbr01 : nbr23) >> (16u * (p & 1u))) & 0xFFFFu;
-                    const bool gi = go && !((ext >> p) & 1u);
-                    sts128_if(gi, sflit + (nb1 * 4u + (p ^ 1u)) * np + nb, f[k]);
-                    sts8_if(gi, reinterpret_cast<uint8_t *>(sfl + nb1 * np + nb) + (p ^ 1u));   // opp(p)
+                    const bool go = ((present >> k) & 1u) && p < 4u && ((intl >> p) & 1u);
+                    const uint32_t w = pick4(na, p & 3u);
+                    sts128_if(go, nf + (w & 0xFFFFu), f[k]);
+                    sts8_if(go, no + (w >> 16));
                 }
             }
+            // (6) the ejected flit (<= 1): its service runs at the start of
+            // the next cycle (after the tile barrier); prefetch what it reads
             if (has_ej) {
-                // while draining, quiescence is judged at the end of each cycle,
-                // so the service is not deferred there
-                if (DRAIN) phase3(S, K, c, ej, t, acc);
-                else { pend = ej; has_pend = true; if (MODE == 1u) prefetch_service(S, c, ej); }
+                const Flit g = pick5(f, (inv >> 16) & 15u);
+                // while draining, quiescence is judged at the end of each
+                // cycle, so the service is not deferred there
+                if (DRAIN) phase3(S, K, c, g, t, acc);
+                else { pend = g; has_pend = true; if (MODE == 1u) prefetch_service(S, c, g); }
             }
             if (DRAIN) busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
