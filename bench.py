@@ -174,12 +174,15 @@ def run_ours(args):
     desc, fn = WORKLOADS[args.workload]
     eng = ENGINES[args.engine]
     cfg = fn(seed=1)
+    scaling = args.scaling or ("strong" if args.workload == "c5" else "weak")
     if world > 1:
-        # weak scaling by row bands (DESIGN 8): the mesh grows to W x (H*N);
-        # rank r owns rows [r*H, (r+1)*H) and exchanges its edge rows' links
-        # with ranks r-1 / r+1 inside the kernel (CUDA IPC over NVLink)
+        # row bands (DESIGN 8): weak scaling grows the mesh to W x (H*N), rank
+        # r owning rows [r*H, (r+1)*H); strong scaling splits the fixed mesh
+        # into N bands.  Edge-row links go to ranks r-1 / r+1 from inside the
+        # kernel (CUDA IPC over NVLink)
         from paper_1508_03235_b200 import dist as pdist
-        cfg["mesh_h"] = cfg["mesh_h"] * world
+        if scaling == "weak":
+            cfg["mesh_h"] = cfg["mesh_h"] * world
         sim = pdist.create_band_sim(cfg, dev, engine=eng)
     else:
         sim = pkg.NocSim(cfg, device=dev, engine=eng)
@@ -241,14 +244,14 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "scaling": scaling, "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (counter-based Philox traffic keyed on (seed, node, cycle))",
         "config": {"workload": args.workload, "desc": desc, "mesh": [cfg["mesh_w"], cfg["mesh_h"]],
                    "nodes_per_gpu": n, "cycles_per_step": cyc, "engine": info1["engine"],
                    "grid": info1["grid"], "block": info1["block"],
                    "l2_flush": "256 MiB buffer written between timed steps" if l2buf is not None else "none",
-                   "parallelism": ("row bands x%d (weak scaling: %dx%d mesh, one %d-row band per GPU, "
-                                   "in-kernel NVLink boundary exchange)" % (world, cfg["mesh_w"], cfg["mesh_h"],
+                   "parallelism": ("row bands x%d (%s scaling: %dx%d mesh, one %d-row band per GPU, "
+                                   "in-kernel NVLink boundary exchange)" % (world, scaling, cfg["mesh_w"], cfg["mesh_h"],
                                                                            cfg["mesh_h"] // world)
                                    if world > 1 else "single GPU")},
         "e2e": {"value": n * cyc * e2e_steps * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -264,10 +267,12 @@ def run_ours(args):
         "sim": {"hash": None, "drops": sum(v for k, v in delta.items() if k.startswith("drops_"))},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt = oracle_rate(cfg, args.cpu_cycles)
+        # bounded sample: at most ~1e8 node-cycles of oracle work
+        ccyc = max(20, min(args.cpu_cycles, int(1e8 // (cfg["mesh_w"] * cfg["mesh_h"]))))
+        v, dt = oracle_rate(cfg, ccyc)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s cycles 0-%d from a fresh state, 1 host thread (%.1f s)" % (
-                                    args.workload, args.cpu_cycles, dt)}
+                                    args.workload, ccyc, dt)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     sim.close()
@@ -289,6 +294,8 @@ def main():
     ap.add_argument("--engine", default="auto", choices=sorted(ENGINES))
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="N>1: weak (mesh height x N, default) or strong (fixed mesh; default for c5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -174,6 +174,17 @@ struct Dev {
     // IPC, when bands are processes).  Null / 0 at the mesh edge.
     unsigned long long *ll_nb[2];
     uint32_t nloc_nb[2];
+    // PERSIST engine with row bands: this band's per-CTA progress counters and
+    // nodes per CTA, and the north (0) / south (1) neighbour band's flit and
+    // flag arrays (by parity), progress counters and nodes per CTA; a link
+    // leaving the band is written into the receiver band's arrays (CUDA IPC
+    // mappings when bands are processes).  Null at the mesh edge.
+    uint32_t *progress;
+    uint32_t npc;
+    uint4 *flit_nb[2][2];
+    uint32_t *flag_nb[2][2];
+    uint32_t *prog_nb[2];
+    uint32_t npc_nb[2];
 };
 
 constexpr uint32_t LL_EMPTY = 0xFFFFFFFFu;   // dst field all ones: never a node (N <= 2^21-1)

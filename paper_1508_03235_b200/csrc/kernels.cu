@@ -61,26 +61,57 @@ __global__ void __launch_bounds__(256) k_step(Dev S, uint64_t t, uint32_t *activ
 }
 
 // ------------------------------------------------------------------ PERSIST engine
+// One cooperative launch for all row bands of this process (DevSet; band k
+// owns CTAs [tile0[k], tile0[k+1])).  Each CTA owns S.npc consecutive nodes of
+// its band and, before each cycle, waits for the CTAs whose nodes lie within
+// one row of its own: in its band (from the second cycle of the launch on) and,
+// at a band edge, in the neighbouring band (from the first cycle on, since
+// that band may still be finishing its previous launch; system scope, since it
+// may be another GPU).  Progress counters count completed cycles (pbase + c + 1).
 // Dynamic shared memory: NCOUNTERS u32 counters, then (optionally) 3*nb u32 bins.
-template <uint32_t MODE>
-__global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, uint32_t ncyc, uint32_t *progress,
-                                                         uint32_t pbase, uint32_t nodes_per_cta, uint32_t smem_hist,
-                                                         uint32_t *activity)
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t *p)
 {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <uint32_t MODE>
+__global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc,
+                                                         uint32_t pbase, uint32_t smem_hist, uint32_t *activity)
+{
+    uint32_t band = 0;
+    while (band + 1 < P.nbands && blockIdx.x >= P.tile0[band + 1]) ++band;
+    __shared__ Dev sD;   // this band's parameters (read every cycle; see tile_engine.cu)
+    for (uint32_t k = threadIdx.x; k < sizeof(Dev) / 4; k += blockDim.x)
+        reinterpret_cast<uint32_t *>(&sD)[k] = reinterpret_cast<const uint32_t *>(&P.d[band])[k];
     extern __shared__ unsigned int sm[];
     unsigned int *scnt = sm;
     unsigned int *shist = smem_hist ? sm + NCOUNTERS : nullptr;
+    __syncthreads();
+    const Dev &S = sD;
     const uint32_t nsm = NCOUNTERS + (smem_hist ? 3u * S.nb : 0u);
     for (uint32_t i = threadIdx.x; i < nsm; i += blockDim.x) sm[i] = 0u;
-    __syncthreads();
 
-    const uint32_t G = gridDim.x, b = blockIdx.x;
-    const uint32_t lo_node = b * nodes_per_cta;
-    const uint32_t hi_node = min(S.nloc, lo_node + nodes_per_cta);
-    // CTAs owning nodes within one row (W) of ours: they feed our input links
-    const uint32_t first = lo_node >= S.W ? (lo_node - S.W) / nodes_per_cta : 0u;
+    const uint32_t G = P.tile0[band + 1] - P.tile0[band], b = blockIdx.x - P.tile0[band];
+    const uint32_t npc = S.npc;
+    uint32_t *const progress = S.progress;
+    const uint32_t lo_node = b * npc;
+    const uint32_t hi_node = min(S.nloc, lo_node + npc);
+    // CTAs of this band owning nodes within one row (W) of ours: they feed our input links
+    const uint32_t first = lo_node >= S.W ? (lo_node - S.W) / npc : 0u;
     const uint32_t lastn = min(S.nloc - 1u, hi_node - 1u + S.W);
-    const uint32_t last = min(G - 1u, lastn / nodes_per_cta);
+    const uint32_t last = min(G - 1u, lastn / npc);
+    // neighbour bands: the CTAs owning the north band's last row / the south band's first row
+    const bool north = lo_node < S.W && S.prog_nb[0] != nullptr;
+    const bool south = hi_node + S.W > S.nloc && S.prog_nb[1] != nullptr;
+    const uint32_t n_first = north ? (S.nloc_nb[0] - S.W) / S.npc_nb[0] : 0u;
+    const uint32_t n_last = north ? (S.nloc_nb[0] - 1u) / S.npc_nb[0] : 0u;
+    const uint32_t s_last = south ? (S.W - 1u) / S.npc_nb[1] : 0u;
     Sink K{scnt, shist, true};
     Acc acc = {0, 0, 0, 0};
     __shared__ int s_abort;
@@ -88,25 +119,29 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, u
     if (threadIdx.x == 0) { s_abort = 0; s_busy[0] = s_busy[1] = 0u; }
     __syncthreads();
 
+    auto wait_for = [&](const uint32_t *prog, uint32_t j, uint32_t target, bool sys) {
+        uint32_t spins = 0;
+        while ((int32_t)((sys ? ld_acquire_sys_u32(&prog[j]) : ld_acquire_u32(&prog[j])) - target) < 0) {
+            if (++spins > (1u << 24)) {   // a hung neighbour: abort the launch, report
+                atomicOr(S.err, 0x80000000u);
+                s_abort = 1;
+                break;
+            }
+        }
+    };
     for (uint32_t c = 0; c < ncyc; ++c) {
         const uint64_t t = t0 + c;
-        if (c > 0) {
-            // wait until every neighbouring CTA completed cycle t-1
-            const uint32_t target = pbase + c;
-            for (uint32_t j = first + threadIdx.x; j <= last; j += blockDim.x) {
-                if (j == b) continue;
-                uint32_t spins = 0;
-                while ((int32_t)(ld_acquire_u32(&progress[j]) - target) < 0) {
-                    if (++spins > (1u << 24)) {   // a hung neighbour: abort the launch, report
-                        atomicOr(S.err, 0x80000000u);
-                        s_abort = 1;
-                        break;
-                    }
-                }
-            }
-            __syncthreads();
-            if (s_abort) break;
-        }
+        const uint32_t target = pbase + c;
+        // wait until every neighbouring CTA completed cycle t-1
+        if (c > 0)
+            for (uint32_t j = first + threadIdx.x; j <= last; j += blockDim.x)
+                if (j != b) wait_for(progress, j, target, false);
+        if (north)
+            for (uint32_t j = n_first + threadIdx.x; j <= n_last; j += blockDim.x) wait_for(S.prog_nb[0], j, target, true);
+        if (south)
+            for (uint32_t j = threadIdx.x; j <= s_last; j += blockDim.x) wait_for(S.prog_nb[1], j, target, true);
+        __syncthreads();
+        if (s_abort) break;
         bool busy = false;
         for (uint32_t l = lo_node + threadIdx.x; l < hi_node; l += blockDim.x)
             busy |= node_step_global<MODE>(S, K, l, t, acc);
@@ -115,8 +150,13 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(Dev S, uint64_t t0, u
         __syncthreads();
         if (threadIdx.x == 0) {
             if (activity && s_busy[c & 1u] == c + 1u) atomicAdd(&activity[c], 1u);
-            __threadfence();
-            st_release_u32(&progress[b], pbase + c + 1u);
+            if (north || south) {   // links written into another band (GPU): system scope
+                __threadfence_system();
+                st_release_sys_u32(&progress[b], pbase + c + 1u);
+            } else {
+                __threadfence();
+                st_release_u32(&progress[b], pbase + c + 1u);
+            }
         }
     }
     flush_acc(S, acc, scnt);
@@ -273,7 +313,10 @@ size_t persist_smem_bytes(const Dev &S, bool with_hist)
     return sizeof(unsigned int) * (NCOUNTERS + (with_hist ? 3u * S.nb : 0u));
 }
 
-cudaError_t persist_configure(const Dev &S, int device, uint32_t *grid, uint32_t *nodes_per_cta, uint32_t *smem_hist)
+// Nodes per CTA and grid for one band with at most max_ctas co-resident CTAs
+// (the whole device divided among the process's bands).
+cudaError_t persist_configure(const Dev &S, int device, uint32_t nbands, uint32_t *grid, uint32_t *nodes_per_cta,
+                              uint32_t *smem_hist)
 {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -289,7 +332,8 @@ cudaError_t persist_configure(const Dev &S, int device, uint32_t *grid, uint32_t
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PERSIST_BLOCK, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    uint64_t max_ctas = (uint64_t)sms * (uint64_t)per_sm;
+    uint64_t max_ctas = (uint64_t)sms * (uint64_t)per_sm / (nbands ? nbands : 1u);
+    if (max_ctas < 1) return cudaErrorInvalidConfiguration;
     uint32_t npc = PERSIST_BLOCK;                     // one node per thread when possible
     uint64_t g = (S.nloc + npc - 1u) / npc;
     if (g > max_ctas) {
@@ -302,16 +346,13 @@ cudaError_t persist_configure(const Dev &S, int device, uint32_t *grid, uint32_t
     return cudaSuccess;
 }
 
-cudaError_t launch_persist(const Dev &S, uint64_t t0, uint32_t ncyc, uint32_t *progress, uint32_t pbase,
-                           uint32_t grid, uint32_t nodes_per_cta, uint32_t smem_hist, uint32_t *activity,
-                           cudaStream_t st)
+cudaError_t launch_persist(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t pbase, uint32_t smem_hist,
+                           uint32_t *activity, cudaStream_t st)
 {
-    size_t smem = persist_smem_bytes(S, smem_hist != 0);
-    Dev Sc = S;
-    void *args[] = {(void *)&Sc, (void *)&t0, (void *)&ncyc, (void *)&progress, (void *)&pbase,
-                    (void *)&nodes_per_cta, (void *)&smem_hist, (void *)&activity};
-    const void *fn = S.mode == 1u ? (const void *)k_persist<1> : (const void *)k_persist<0>;
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(PERSIST_BLOCK), args, smem, st);
+    size_t smem = persist_smem_bytes(P.d[0], smem_hist != 0);
+    void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&pbase, (void *)&smem_hist, (void *)&activity};
+    const void *fn = P.d[0].mode == 1u ? (const void *)k_persist<1> : (const void *)k_persist<0>;
+    return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(PERSIST_BLOCK), args, smem, st);
 }
 
 cudaError_t launch_busy_count(const Dev &S, uint64_t t, uint32_t *out, cudaStream_t st)

@@ -39,11 +39,10 @@ cudaError_t launch_tiled4(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t 
 cudaError_t launch_ll_reset(const Dev &S, uint64_t t, cudaStream_t st);
 
 cudaError_t launch_step(const Dev &S, uint64_t t, uint32_t *activity, cudaStream_t st);
-cudaError_t persist_configure(const Dev &S, int device, uint32_t *grid, uint32_t *nodes_per_cta,
+cudaError_t persist_configure(const Dev &S, int device, uint32_t nbands, uint32_t *grid, uint32_t *nodes_per_cta,
                               uint32_t *smem_hist);
-cudaError_t launch_persist(const Dev &S, uint64_t t0, uint32_t ncyc, uint32_t *progress, uint32_t pbase,
-                           uint32_t grid, uint32_t nodes_per_cta, uint32_t smem_hist, uint32_t *activity,
-                           cudaStream_t st);
+cudaError_t launch_persist(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t pbase, uint32_t smem_hist,
+                           uint32_t *activity, cudaStream_t st);
 cudaError_t launch_busy_count(const Dev &S, uint64_t t, uint32_t *out, cudaStream_t st);
 cudaError_t launch_hash(const Dev &S, uint64_t t, unsigned long long *out, cudaStream_t st);
 

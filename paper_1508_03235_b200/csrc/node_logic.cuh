@@ -673,16 +673,27 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
         const uint32_t nf = __popc(in.present);
         const uint8_t st1 = stamp_of(t + 1);
         route(S, c, in, t, acc, ej, has_ej, [&](uint32_t p, const Flit &f) {
-            // neighbour's local index and its input slot opp(p)
-            uint32_t m, slot;
+            // neighbour's local index and its input slot opp(p); a link that
+            // leaves the row band lands in the neighbour band's arrays (DESIGN 8)
+            uint32_t m, slot, nl = S.nloc;
+            uint4 *fl = S.flit[nb1];
+            uint32_t *fg = S.flag[nb1];
             switch (p) {
-            case PN: m = l - S.W; slot = PS; break;
-            case PS: m = l + S.W; slot = PN; break;
+            case PN:
+                slot = PS;
+                if (l < S.W) { nl = S.nloc_nb[0]; m = l - S.W + nl; fl = S.flit_nb[0][nb1]; fg = S.flag_nb[0][nb1]; }
+                else m = l - S.W;
+                break;
+            case PS:
+                slot = PN;
+                if (l + S.W >= S.nloc) { nl = S.nloc_nb[1]; m = l + S.W - S.nloc; fl = S.flit_nb[1][nb1]; fg = S.flag_nb[1][nb1]; }
+                else m = l + S.W;
+                break;
             case PE: m = l + 1u; slot = PW; break;
             default: m = l - 1u; slot = PE; break;
             }
-            S.flit[nb1][(size_t)slot * S.nloc + m] = make_uint4(f.x, f.y, f.z, f.w);
-            reinterpret_cast<uint8_t *>(S.flag[nb1])[(size_t)m * 4u + slot] = st1;
+            fl[(size_t)slot * nl + m] = make_uint4(f.x, f.y, f.z, f.w);
+            reinterpret_cast<uint8_t *>(fg)[(size_t)m * 4u + slot] = st1;
         });
         c.busy_flit = nf > (has_ej ? 1u : 0u);
     }

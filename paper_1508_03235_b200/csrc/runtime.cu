@@ -291,6 +291,53 @@ static int link_ranks(noc_sim *s)
     return NOC_OK;
 }
 
+// multi-GPU, PERSIST engine: map the neighbour bands' flit / flag arrays (both
+// parities) and progress counters, and learn their nodes per CTA
+static int link_ranks_persist(noc_sim *s)
+{
+    Dev &D = s->D[0];
+    const int NH = 5;   // flit[0], flit[1], flag[0], flag[1], progress
+    void *mine_p[NH] = {D.flit[0], D.flit[1], D.flag[0], D.flag[1], D.progress};
+    uint8_t rec[NH * 64 + 8];
+    memset(rec, 0, sizeof rec);
+    for (int i = 0; i < NH; ++i) {
+        cudaIpcMemHandle_t h;
+        CU(cudaIpcGetMemHandle(&h, mine_p[i]));
+        memcpy(rec + 64 * i, &h, 64);
+    }
+    memcpy(rec + NH * 64, &D.npc, 4);
+    const size_t R = sizeof rec;
+    uint8_t *dev_h = nullptr;
+    int rc;
+    if ((rc = dalloc(s, &dev_h, R * s->world))) return rc;
+    CU(cudaMemcpy(dev_h + R * s->rank, rec, R, cudaMemcpyHostToDevice));
+    NC(ncclAllGather(dev_h + R * s->rank, dev_h, R, ncclUint8, s->comm, s->stream));
+    std::vector<uint8_t> all(R * s->world);
+    CU(cudaMemcpyAsync(all.data(), dev_h, all.size(), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    for (int side = 0; side < 2; ++side) {
+        const int r = side == 0 ? s->rank - 1 : s->rank + 1;
+        if (r < 0 || r >= s->world) continue;
+        void *p[NH];
+        for (int i = 0; i < NH; ++i) {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, all.data() + R * r + 64 * i, 64);
+            CU(cudaIpcOpenMemHandle(&p[i], h, cudaIpcMemLazyEnablePeerAccess));
+            s->ipc_opened.push_back(p[i]);
+        }
+        uint32_t row0, rows;
+        band_rows(D.H, s->P, r, &row0, &rows);
+        D.flit_nb[side][0] = (uint4 *)p[0];
+        D.flit_nb[side][1] = (uint4 *)p[1];
+        D.flag_nb[side][0] = (uint32_t *)p[2];
+        D.flag_nb[side][1] = (uint32_t *)p[3];
+        D.prog_nb[side] = (uint32_t *)p[4];
+        memcpy(&D.npc_nb[side], all.data() + R * r + NH * 64, 4);
+        D.nloc_nb[side] = rows * D.W;
+    }
+    return NOC_OK;
+}
+
 extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
 {
     if (!out) return fail(NOC_EINVAL, "null out");
@@ -334,10 +381,9 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         if ((rc = make_band(s, cfg, s->g0 + k, s->D[k]))) return bail(rc);
 
     // engine: TILED when every band's tiles fit one CTA of <= TILE_BLOCK_MAX
-    // threads per SM, else PERSIST (DESIGN 6.2); bands require TILED
+    // threads per SM, else PERSIST (DESIGN 6.2); bands need TILED or PERSIST
     s->engine = cfg->engine;
-    if (s->P > 1 && s->engine != NOC_ENGINE_AUTO && s->engine != NOC_ENGINE_TILED && s->engine != NOC_ENGINE_TILED4)
-        return bail(fail(NOC_EINVAL, "row bands need a TILED engine"));
+    if (s->P > 1 && s->engine == NOC_ENGINE_STEP) return bail(fail(NOC_EINVAL, "row bands need the TILED or PERSIST engine"));
     // AUTO tries TILED (one thread per node), then TILED4 (4 lanes per node,
     // 2 CTAs per SM), then PERSIST: TILED is the fastest at the bench size
     // (DESIGN 6.4, profiles/r01_ab_engines.txt)
@@ -369,10 +415,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         if (s->engine == cand)
             return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") + cudaGetErrorString(ce)));
     }
-    if (s->engine == NOC_ENGINE_AUTO) {
-        if (s->P > 1) return bail(fail(NOC_EINVAL, "row bands do not fit a TILED engine"));
-        s->engine = NOC_ENGINE_PERSIST;
-    }
+    if (s->engine == NOC_ENGINE_AUTO) s->engine = NOC_ENGINE_PERSIST;
     if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
         for (int k = 0; k < s->nb; ++k)
             if ((rc = dalloc(s, &s->D[k].ll, (size_t)32u * s->D[k].nloc))) return bail(rc);
@@ -391,9 +434,36 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         }
     }
     if (s->engine == NOC_ENGINE_PERSIST) {
-        cudaError_t ce = persist_configure(s->D[0], s->device, &s->p_grid, &s->p_npc, &s->p_smem_hist);
-        if (ce != cudaSuccess) return bail(fail(NOC_ECUDA, std::string("persist_configure: ") + cudaGetErrorString(ce)));
-        if ((rc = dalloc(s, &s->progress, s->p_grid))) return bail(rc);
+        // each band: its CTAs, nodes per CTA and progress counters; then the
+        // neighbour bands' link arrays and progress (in-process, or CUDA IPC)
+        s->set.nbands = (uint32_t)s->nb;
+        s->set.tile0[0] = 0;
+        for (int k = 0; k < s->nb; ++k) {
+            uint32_t g = 0, npc = 0;
+            cudaError_t ce = persist_configure(s->D[k], s->device, (uint32_t)s->nb, &g, &npc, &s->p_smem_hist);
+            if (ce != cudaSuccess) return bail(fail(NOC_ECUDA, std::string("persist_configure: ") + cudaGetErrorString(ce)));
+            s->D[k].npc = npc;
+            if ((rc = dalloc(s, &s->D[k].progress, g))) return bail(rc);
+            s->set.tile0[k + 1] = s->set.tile0[k] + g;
+        }
+        s->p_grid = s->set.tile0[s->nb];
+        s->p_npc = s->D[0].npc;
+        s->progress = s->D[0].progress;
+        if (s->world > 1) {
+            if ((rc = link_ranks_persist(s))) return bail(rc);
+        } else {
+            for (int k = 0; k < s->nb; ++k)
+                for (int side = 0; side < 2; ++side) {
+                    const int j = side == 0 ? k - 1 : k + 1;
+                    if (j < 0 || j >= s->nb) continue;
+                    Dev &D = s->D[k], &E = s->D[j];
+                    for (int b = 0; b < 2; ++b) { D.flit_nb[side][b] = E.flit[b]; D.flag_nb[side][b] = E.flag[b]; }
+                    D.prog_nb[side] = E.progress;
+                    D.npc_nb[side] = E.npc;
+                    D.nloc_nb[side] = E.nloc;
+                }
+        }
+        for (int k = 0; k < s->nb; ++k) s->set.d[k] = s->D[k];
     }
     if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(NOC_ECUDA, "init sync failed"));
     if (s->world > 1) {   // every rank has mapped its neighbours before anyone runs
@@ -456,8 +526,8 @@ static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
-            e = launch_persist(s->D[0], s->t + done, k, s->progress, s->pbase, s->p_grid, s->p_npc, s->p_smem_hist,
-                               activity ? activity + done : nullptr, s->stream);
+            e = launch_persist(s->set, s->t + done, k, s->pbase, s->p_smem_hist, activity ? activity + done : nullptr,
+                               s->stream);
             if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
             s->pbase += k;
             done += k;

@@ -230,7 +230,7 @@ def test_c3_drain_window(engine):
         assert_same(g, o)
 
 
-@pytest.mark.parametrize("engine", TILED_ENGINES)
+@pytest.mark.parametrize("engine", TILED_ENGINES + [nb.ENGINE_PERSIST])
 @pytest.mark.parametrize("bands", [2, 3, 5, 8])
 @pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
 def test_virtual_bands_match_oracle(bands, mode, engine):
@@ -258,4 +258,32 @@ def test_virtual_bands_c3():
     o = Oracle(cfg)
     g.run(1000)
     o.run(1000)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("mode", [W.MODE_LSPD, W.MODE_UR])
+def test_c5_1024x1024(mode):
+    """BASELINE configs[4] on one GPU (1,048,576 nodes; AUTO picks PERSIST,
+    more than 512 nodes per SM): 300 cycles bit-exact against the oracle,
+    then the state after a drain window."""
+    cfg = W.c5(mode=mode)
+    g, o = both(cfg, 300)
+    assert g.info()["engine"] == nb.ENGINE_PERSIST
+    assert_same(g, o)
+    assert g.drain(20) == o.drain(20)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("bands", [2, 4, 8])
+def test_c5_virtual_bands(bands):
+    """BASELINE configs[4] partitioned into 1024/P-row bands (the 2/4/8-GPU
+    decomposition, DESIGN 8) on one GPU: PERSIST bands, band-edge links written
+    into the neighbour band's arrays, bit-exact against the oracle."""
+    cfg = W.c5()
+    g = nb.NocSim(cfg, bands=bands)
+    assert g.info()["engine"] == nb.ENGINE_PERSIST
+    o = Oracle(cfg)
+    for k in (150, 150):
+        g.run(k)
+        o.run(k)
     assert_same(g, o)
