@@ -48,6 +48,13 @@ extern "C" {
 /* router priority (DESIGN R1) */
 #define NOC_PRIO_DEFLECT 0u /* age = deflection count      */
 #define NOC_PRIO_OLDEST  1u /* oldest injection cycle first            */
+
+/* routing (DESIGN R3, R5; SURVEY 8(f) NEXT-f4 compatibility mode) */
+#define NOC_ROUTE_PMDR   0u /* productive ports x then y; deflect to the first free
+                               existing port in N,S,E,W         */
+#define NOC_ROUTE_XY     1u /* strict XY: the x-port while dx != 0, then the
+                               y-port; deflect in N,E,S,W order (SPEC S:L136,
+                               S:L162)                                         */
 /* engine: which kernel organisation advances the cycles.  Results are
  * bit-identical for every engine. */
 #define NOC_ENGINE_AUTO     0u  /* library picks                                 */
@@ -95,7 +102,8 @@ typedef struct noc_sim_config {
                                   many row bands on one GPU ("virtual bands", the
                                   multi-GPU partition on one device); 0/1 = none.
                                   Results are identical for every value.         */
-    uint32_t reserved[7];      /* must be 0                                        */
+    uint32_t route;            /* NOC_ROUTE_* (0 = the paper's reading)           */
+    uint32_t reserved[6];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list

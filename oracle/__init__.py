@@ -56,7 +56,7 @@ class _Config(C.Structure):
         ("priv_tags", C.c_uint32), ("thr_inj", C.c_uint32), ("thr_priv", C.c_uint32),
         ("l2_hit_lat", C.c_uint32), ("mem_lat", C.c_uint32), ("nfl_ra", C.c_uint32),
         ("sendq_cap", C.c_uint32), ("hist_bins", C.c_uint32), ("seed", C.c_uint64),
-        ("script", C.POINTER(_Event)), ("n_script", C.c_uint64),
+        ("script", C.POINTER(_Event)), ("n_script", C.c_uint64), ("route", C.c_uint32),
     ]
 
 
@@ -84,7 +84,7 @@ def lib():
         L.orc_state_hash.restype = C.c_uint64
         L.orc_last_error.restype = C.c_char_p
         L.orc_philox.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
-        L.orc_arbitrate.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+        L.orc_arbitrate.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_int),
                                     C.POINTER(C.c_uint64)]
         L.orc_links_occupied.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
@@ -122,9 +122,10 @@ def philox(key, ctr):
     return tuple(o)
 
 
-def arbitrate(mesh_w, mesh_h, node, prio, flits):
+def arbitrate(mesh_w, mesh_h, node, prio, flits, route=0):
     """One router decision.  flits = [(dst, src, age, inj), ...].
-    Returns ([port...], [age_after...]); port 0..3 = N,S,E,W, 4 = eject."""
+    Returns ([port...], [age_after...]); port 0..3 = N,S,E,W, 4 = eject.
+    route: 0 = PMDR (R3, R5), 1 = strict XY with N,E,S,W deflection (NEXT-f4)."""
     nf = len(flits)
     arr = (C.c_uint64 * (4 * max(nf, 1)))()
     for i, f in enumerate(flits):
@@ -132,7 +133,7 @@ def arbitrate(mesh_w, mesh_h, node, prio, flits):
             arr[4 * i + j] = f[j]
     ports = (C.c_int * 5)()
     ages = (C.c_uint64 * 5)()
-    rc = lib().orc_arbitrate(mesh_w, mesh_h, node, prio, nf, arr, ports, ages)
+    rc = lib().orc_arbitrate(mesh_w, mesh_h, node, prio, route, nf, arr, ports, ages)
     if rc != 0:
         raise ValueError("more flits than router degree")
     return list(ports[:nf]), list(ages[:nf])

@@ -421,7 +421,7 @@ static int ranks_before(uint32_t prio, const ArbFlit *a, const ArbFlit *b)
 
 /* Router decision for flits F[0..nf-1] at node n.  Writes port[i] and
  * deflected[i].  Returns -1 if nf exceeds the degree. */
-static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t nf,
+static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t route, uint32_t nf,
                      const ArbFlit *F, int *port, int *deflected)
 {
     uint32_t order[5];
@@ -451,14 +451,15 @@ static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t
             eject_taken = 1;
             continue;
         }
-        if (f->dst != n) {                         /* PMDR: x first, then y (R3) */
+        if (f->dst != n) {
             uint32_t dx = f->dst % W, dy = f->dst / W;
             int p = -1;
-            if (dx != x) {
+            if (dx != x) {                         /* PMDR: x first, then y (R3) */
                 int xp = dx > x ? DIR_E : DIR_W;
                 if (!used[xp]) p = xp;
             }
-            if (p < 0 && dy != y) {
+            /* strict XY: the y-port is preferred only once dx = 0 */
+            if (p < 0 && dy != y && (route == ORC_ROUTE_PMDR || dx == x)) {
                 int yp = dy > y ? DIR_S : DIR_N;
                 if (!used[yp]) p = yp;
             }
@@ -468,8 +469,13 @@ static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t
                 continue;
             }
         }
-        /* deflection: first free existing port in N,S,E,W (R4, R5) */
-        for (int d = 0; d < 4; ++d) {
+        /* deflection: first free existing port in N,S,E,W (R4, R5), or in
+         * N,E,S,W under the strict-XY mode */
+        static const int scan_pmdr[4] = { DIR_N, DIR_S, DIR_E, DIR_W };
+        static const int scan_xy[4] = { DIR_N, DIR_E, DIR_S, DIR_W };
+        const int *scan = route == ORC_ROUTE_XY ? scan_xy : scan_pmdr;
+        for (int k2 = 0; k2 < 4; ++k2) {
+            const int d = scan[k2];
             if (has_nbr(W, H, n, d) && !used[d]) {
                 used[d] = 1;
                 port[i] = d;
@@ -481,7 +487,7 @@ static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t
     return 0;
 }
 
-int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio,
+int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
                   uint32_t nf, const uint64_t *flits, int *out_port, uint64_t *out_age)
 {
     ArbFlit F[5] = {{0, 0, 0, 0}};
@@ -493,7 +499,7 @@ int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio
         F[i].age = flits[4 * i + 2];
         F[i].inj = flits[4 * i + 3];
     }
-    if (arbitrate(mesh_w, mesh_h, node, prio, nf, F, out_port, defl) != 0) return -1;
+    if (arbitrate(mesh_w, mesh_h, node, prio, route, nf, F, out_port, defl) != 0) return -1;
     for (uint32_t i = 0; i < nf; ++i) out_age[i] = F[i].age + (uint64_t)defl[i];
     return 0;
 }
@@ -537,7 +543,7 @@ static void phase2(orc_sim *s, uint32_t n)
         A[i].dst = F[i].dst; A[i].src = F[i].src; A[i].age = F[i].age; A[i].inj = F[i].inj;
         if (s->t - F[i].inj > LIFE_MAX) fail(s, ORC_EOVERFLOW, "flit lifetime overflow");
     }
-    if (arbitrate(s->W, s->H, n, s->cfg.prio, nf, A, port, defl) != 0) {
+    if (arbitrate(s->W, s->H, n, s->cfg.prio, s->cfg.route, nf, A, port, defl) != 0) {
         fail(s, ORC_EASSERT, "more flits than ports at a router");
         return;
     }
@@ -720,7 +726,7 @@ int orc_create(const orc_config *cfg, orc_sim **out)
     if (W < 2 || H < 2 || W > 2048 || H > 2048 || (uint64_t)W * H > (1u << 21)) {
         set_err("mesh must be 2..2048 per side and at most 2^21 nodes"); return ORC_EINVAL;
     }
-    if (cfg->mode > 1 || cfg->prio > 1) { set_err("bad mode/prio"); return ORC_EINVAL; }
+    if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1) { set_err("bad mode/prio/route"); return ORC_EINVAL; }
     if (cfg->sendq_cap == 0 || cfg->sendq_cap > 1024 || (cfg->sendq_cap & (cfg->sendq_cap - 1))) {
         set_err("sendq_cap must be a power of two in 1..1024"); return ORC_EINVAL;
     }

@@ -32,6 +32,9 @@ extern "C" {
 /* priority (R1) */
 #define ORC_PRIO_DEFLECT 0 /* age = #deflections       */
 #define ORC_PRIO_OLDEST  1 /* oldest injection cycle first         */
+/* routing (R3, R5; NEXT-f4 compatibility mode) */
+#define ORC_ROUTE_PMDR   0 /* productive ports x then y, deflect in N,S,E,W */
+#define ORC_ROUTE_XY     1 /* SPEC: strict XY preference, deflect in N,E,S,W  */
 
 /* debug flags for orc_set_debug */
 #define ORC_DBG_REVERSE    1  /* iterate nodes in reverse order in every phase */
@@ -60,6 +63,7 @@ typedef struct {
     uint64_t seed;
     const orc_event *script;     /* optional, may be NULL                   */
     uint64_t n_script;
+    uint32_t route;              /* ORC_ROUTE_*                             */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */
@@ -94,7 +98,7 @@ void orc_philox(uint32_t k0, uint32_t k1, const uint32_t c[4], uint32_t out[4]);
  *   out_port[i]: 0..3 = N,S,E,W output, 4 = eject
  *   out_age[i] : age after the decision
  * Returns 0, or -1 if nf > degree. */
-int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio,
+int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
                   uint32_t nf, const uint64_t *flits, int *out_port,
                   uint64_t *out_age);
 

@@ -142,7 +142,7 @@ enum : uint64_t { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, 
 struct Dev {
     // geometry and model parameters
     uint32_t W, H, N, n0, nloc, row0, rows;
-    uint32_t mode, prio, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
+    uint32_t mode, prio, route, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
     uint32_t qcap, nb, seed_lo, seed_hi;
     uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi
     uint32_t gen;                     // generation enabled (0 during drain)
@@ -186,6 +186,17 @@ struct Dev {
     uint32_t *prog_nb[2];
     uint32_t npc_nb[2];
 };
+
+// Deflection port: the first free existing port in N,S,E,W (R5), or in
+// N,E,S,W under the strict-XY mode (route 1).  freem != 0.
+__device__ __forceinline__ uint32_t defl_port(uint32_t freem, uint32_t route)
+{
+    if (route == 0u) return (uint32_t)(__ffs(freem) - 1);
+    if (freem & 1u) return PN;
+    if (freem & 4u) return PE;
+    if (freem & 2u) return PS;
+    return PW;
+}
 
 constexpr uint32_t LL_EMPTY = 0xFFFFFFFFu;   // dst field all ones: never a node (N <= 2^21-1)
 

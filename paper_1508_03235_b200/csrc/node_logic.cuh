@@ -512,13 +512,13 @@ __device__ __forceinline__ uint32_t route_select(const Dev &S, const NodeCtx &c,
                 const uint32_t xp = dx > c.x ? PE : PW;
                 if (!(used & (1u << xp))) p = (int)xp;
             }
-            if (p < 0 && dy != c.y) {
+            if (p < 0 && dy != c.y && (S.route == 0u || dx == c.x)) {   // strict XY: y only once dx = 0
                 const uint32_t yp = dy > c.y ? PS : PN;
                 if (!(used & (1u << yp))) p = (int)yp;
             }
         }
         if (p < 0) {
-            p = (int)(__ffs(exist & ~used) - 1);     // first free existing port in N,S,E,W (R5)
+            p = (int)defl_port(exist & ~used, S.route);   // first free existing port in N,S,E,W (R5) / N,E,S,W (XY)
             uint32_t a = f_age(f) + 1u;
             if (a > AGE_MAX) { atomicOr(S.err, ERR_AGE); a = AGE_MAX; }
             f_set_age(f, a);

@@ -108,7 +108,7 @@ static int validate(const noc_sim_config *c)
     const uint64_t N = (uint64_t)c->mesh_w * c->mesh_h;
     if (c->mesh_w < 2 || c->mesh_h < 2 || c->mesh_w > 2048 || c->mesh_h > 2048 || N > (1u << 21) - 1u)
         return fail(NOC_EINVAL, "mesh must be 2..2048 per side and at most 2^21-1 nodes (R9, R32)");
-    if (c->mode > 1 || c->prio > 1) return fail(NOC_EINVAL, "mode/prio out of range");
+    if (c->mode > 1 || c->prio > 1 || c->route > 1) return fail(NOC_EINVAL, "mode/prio/route out of range");
     if (c->sendq_cap == 0 || c->sendq_cap > 1024 || (c->sendq_cap & (c->sendq_cap - 1)))
         return fail(NOC_EINVAL, "sendq_cap must be a power of two in 1..1024");
     if (c->hist_bins == 0 || c->hist_bins > 65536) return fail(NOC_EINVAL, "hist_bins must be 1..65536");
@@ -129,7 +129,7 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    for (int i = 0; i < 7; ++i)
+    for (int i = 0; i < 6; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->n_script && !c->script) return fail(NOC_EINVAL, "n_script > 0 with a null script");
     for (uint64_t i = 0; i < c->n_script; ++i) {
@@ -181,6 +181,7 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.nloc = D.rows * D.W;
     D.mode = cfg->mode;
     D.prio = cfg->prio;
+    D.route = cfg->route;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;

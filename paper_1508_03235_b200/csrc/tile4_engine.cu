@@ -300,7 +300,7 @@ k_tiled4(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t 
                 } else {
                     const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
                     if (dx != c.x) pref |= 4u | ((dx > c.x ? PE : PW) << 3);
-                    if (dy != c.y) pref |= 32u | ((dy > c.y ? PS : PN) << 6);
+                    if (dy != c.y && (S.route == 0u || dx == c.x)) pref |= 32u | ((dy > c.y ? PS : PN) << 6);
                 }
             }
             const uint32_t word = pref | (rank << 8);
@@ -326,7 +326,7 @@ k_tiled4(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t 
                             else if ((sel & 32u) && !((u >> yp) & 1u)) p = yp;
                         }
                         if (p == NOPORT) {
-                            p = __ffs(exist & ~u) - 1u;   // first free existing port in N,S,E,W (R5)
+                            p = defl_port(exist & ~u, S.route);   // first free existing port, N,S,E,W (R5) / N,E,S,W (XY)
                             dmask |= 1u << lk;
                         }
                         u |= 1u << p;

@@ -572,7 +572,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     const uint32_t xp = dx > c.x ? PE : PW, yp = dy > c.y ? PS : PN;
                     const uint32_t pw = dst == c.n ? 1u
                                                    : ((dx != c.x ? 2u | (xp << 2) : 0u) |
-                                                      (dy != c.y ? 16u | (yp << 5) : 0u));
+                                                      (dy != c.y && (S.route == 0u || dx == c.x) ? 16u | (yp << 5) : 0u));
                     prefs |= (uint64_t)pw << (8u * k);
                     if (k < 4) {
                         const uint32_t life = st - f[k].z;
@@ -610,7 +610,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     } else {
                         if ((pw & 2u) && !((used >> xp) & 1u)) p = xp;
                         else if ((pw & 16u) && !((used >> yp) & 1u)) p = yp;
-                        else { p = __ffs(exist & ~used) - 1u; dm |= 1u << k; }
+                        else { p = defl_port(exist & ~used, S.route); dm |= 1u << k; }
                         used |= 1u << p;
                     }
                     ports |= p << (4u * k);

@@ -14,6 +14,7 @@ from fractions import Fraction
 
 MODE_UR, MODE_LSPD = 0, 1
 PRIO_DEFLECT, PRIO_OLDEST = 0, 1
+ROUTE_PMDR, ROUTE_XY = 0, 1   # NEXT-f4: strict XY + N,E,S,W deflection
 
 
 def thr(p) -> int:
@@ -28,7 +29,7 @@ BASE = dict(
     tags_per_node=128, priv_tags=96,
     thr_inj=thr(0.1), thr_priv=thr(0.5),
     l2_hit_lat=1, mem_lat=100, nfl_ra=4,
-    sendq_cap=16, hist_bins=4096, seed=1,
+    sendq_cap=16, hist_bins=4096, seed=1, route=0,
 )
 
 

@@ -287,3 +287,30 @@ def test_c5_virtual_bands(bands):
         g.run(k)
         o.run(k)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("cfg", [
+    W.c1a(route=W.ROUTE_XY, lam=0.3),
+    W.c1b(route=W.ROUTE_XY, seed=2),
+    W.make(mesh_w=16, mesh_h=16, mode=W.MODE_UR, lam=0.4, route=W.ROUTE_XY, prio=W.PRIO_OLDEST),
+    W.lspd(24, 20, lam=0.2, route=W.ROUTE_XY),
+], ids=["c1a", "c1b", "ur16_oldest", "lspd24x20"])
+def test_strict_xy_compat_mode(cfg, engine):
+    """NEXT-f4: SPEC's strict-XY preference with N,E,S,W deflection scan, on
+    every engine, bit-exact against the oracle (saturated UR exercises the
+    deflection order)."""
+    g, o = both(cfg, 3000, engine)
+    assert_same(g, o)
+    assert g.stats()[0]["deflections"] > 0
+
+
+def test_strict_xy_c3_and_bands():
+    cfg = W.c3(route=W.ROUTE_XY)
+    g, o = both(cfg, 800)
+    assert_same(g, o)
+    g = nb.NocSim(W.lspd(22, 19, lam=0.3, route=W.ROUTE_XY), bands=3)
+    o = Oracle(W.lspd(22, 19, lam=0.3, route=W.ROUTE_XY))
+    g.run(1500)
+    o.run(1500)
+    assert_same(g, o)

@@ -129,19 +129,25 @@ def productive(w, n, dst):
     return ports
 
 
-def brute_force(w, h, n, prio, flits):
+def brute_force(w, h, n, prio, flits, route=W.ROUTE_PMDR):
     """Lexicographically least vector of preference indices, in rank order,
     over all injective assignments (serial dictatorship): found by a
-    depth-first search that tries options in preference order."""
+    depth-first search that tries options in preference order.  Preference
+    lists: PMDR (R3, R5) = productive ports x then y, then the other existing
+    ports in N,S,E,W; strict XY (NEXT-f4) = the XY port,
+    then the other existing ports in N,E,S,W."""
     order = sorted(range(len(flits)), key=lambda i: rank_key(flits[i], prio))
+    scan = (N_, S_, E_, W_) if route == W.ROUTE_PMDR else (N_, E_, S_, W_)
     prefs = []
     for i in order:
         dst = flits[i][0]
         if dst == n:
-            lst = [X_] + [p for p in (N_, S_, E_, W_) if exists(w, h, n, p)]
+            lst = [X_] + [p for p in scan if exists(w, h, n, p)]
         else:
             lst = productive(w, n, dst)
-            lst += [p for p in (N_, S_, E_, W_) if exists(w, h, n, p) and p not in lst]
+            if route == W.ROUTE_XY:
+                lst = lst[:1]
+            lst += [p for p in scan if exists(w, h, n, p) and p not in lst]
         prefs.append(lst)
     assign = [None] * len(order)
 
@@ -161,15 +167,16 @@ def brute_force(w, h, n, prio, flits):
     for k, i in enumerate(order):
         p = assign[k]
         dst = flits[i][0]
-        ok = (p == X_) if dst == n else (p in productive(w, n, dst))
+        good = productive(w, n, dst) if route == W.ROUTE_PMDR else productive(w, n, dst)[:1]
+        ok = (p == X_) if dst == n else (p in good)
         ports[i] = p
         ages[i] = flits[i][2] + (0 if ok else 1)
     return ports, ages
 
 
-def check_case(w, h, n, prio, flits):
-    got = oracle.arbitrate(w, h, n, prio, flits)
-    assert got == brute_force(w, h, n, prio, flits), (w, h, n, prio, flits)
+def check_case(w, h, n, prio, flits, route=W.ROUTE_PMDR):
+    got = oracle.arbitrate(w, h, n, prio, flits, route)
+    assert got == brute_force(w, h, n, prio, flits, route), (w, h, n, prio, flits, route)
     ports = got[0]
     assert len(set(ports)) == len(ports)                         # one flit per port
     assert all(p == X_ or exists(w, h, n, p) for p in ports)     # never off the mesh
@@ -187,8 +194,18 @@ def test_arbitration_hand_cases():
         assert got[1] == [int(a) for a in ages.split()], case
 
 
+def test_arbitration_hand_cases_strict_xy():
+    """NEXT-f4 compatibility mode against hand-worked decisions."""
+    for case, node, fl, ports, ages, route in golden("arbitration_cases_xy.txt"):
+        flits = [tuple(int(v) for v in f.split(",")) for f in fl.split(";")]
+        got = oracle.arbitrate(3, 3, int(node), W.PRIO_DEFLECT, flits, int(route))
+        assert got[0] == [PORT[p] for p in ports.split()], case
+        assert got[1] == [int(a) for a in ages.split()], case
+
+
+@pytest.mark.parametrize("route", [W.ROUTE_PMDR, W.ROUTE_XY])
 @pytest.mark.parametrize("prio", [W.PRIO_DEFLECT, W.PRIO_OLDEST])
-def test_arbitration_exhaustive_corner(prio):
+def test_arbitration_exhaustive_corner(prio, route):
     """Every degree-2 case at the 3x3 corner (0,0): each input empty or a flit
     with dst in 9 nodes x age 0..2 x inj 0..1, both src orders, plus the
     injected flit (age 0, inj 2) whenever an input is free (R7)."""
@@ -205,14 +222,15 @@ def test_arbitration_exhaustive_corner(prio):
                 flits = base + ([(inj, n, 0, 2)] if inj is not None else [])
                 if not flits:
                     continue
-                check_case(w, h, n, prio, flits)
+                check_case(w, h, n, prio, flits, route)
                 count += 1
     assert count > 5000
 
 
+@pytest.mark.parametrize("route", [W.ROUTE_PMDR, W.ROUTE_XY])
 @pytest.mark.parametrize("prio", [W.PRIO_DEFLECT, W.PRIO_OLDEST])
 @pytest.mark.parametrize("node", [1, 4])
-def test_arbitration_random_edge_and_centre(prio, node):
+def test_arbitration_random_edge_and_centre(prio, node, route):
     """Degree-3 (edge) and degree-4 (centre) routers of a 3x3 mesh: random
     cases against the brute force."""
     rng = random.Random(1000 + node + 10 * prio)
@@ -225,7 +243,7 @@ def test_arbitration_random_edge_and_centre(prio, node):
         if k < deg and rng.random() < 0.7:
             flits.append((rng.randrange(9), node, 0, 2))
         if flits:
-            check_case(w, h, node, prio, flits)
+            check_case(w, h, node, prio, flits, route)
 
 
 def test_arbitration_rejects_overfull_router():
@@ -241,6 +259,10 @@ INV_CFGS = [
     ("lspd4x4_oldest", W.c1b(prio=W.PRIO_OLDEST, seed=3)),
     ("lspd6x5", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.2,
                        sendq_cap=32, seed=2, mem_lat=30)),
+    # NEXT-f4 strict-XY compatibility mode
+    ("ur5x3_xy", W.make(mesh_w=5, mesh_h=3, mode=W.MODE_UR, lam=0.3, route=W.ROUTE_XY)),
+    ("lspd6x5_xy", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.2,
+                          sendq_cap=32, seed=2, mem_lat=30, route=W.ROUTE_XY)),
 ]
 
 
