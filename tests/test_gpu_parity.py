@@ -314,3 +314,12 @@ def test_strict_xy_c3_and_bands():
     g.run(1500)
     o.run(1500)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("mode,lam", [(W.MODE_UR, 0.05), (W.MODE_UR, 0.5), (W.MODE_LSPD, 0.05),
+                                      (W.MODE_LSPD, 0.5)])
+def test_c4_sweep_endpoints(mode, lam):
+    """BASELINE configs[3]: the ends of the 208x208 injection sweep (AUTO
+    engine) bit-exact against the oracle."""
+    g, o = both(W.c4(lam, mode=mode), 600)
+    assert_same(g, o)
