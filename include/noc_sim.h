@@ -49,6 +49,11 @@ extern "C" {
 #define NOC_PRIO_DEFLECT 0u /* age = deflection count      */
 #define NOC_PRIO_OLDEST  1u /* oldest injection cycle first            */
 
+/* directory organisation (DESIGN R12, R40) */
+#define NOC_DIR_DISTRIBUTED 0u /* home(T) = T mod N (R12)                          */
+#define NOC_DIR_CENTRAL     1u /* home(T) = dir_node for every T: the paper's
+                                  centralized location array     */
+
 /* routing (DESIGN R3, R5; SURVEY 8(f) NEXT-f4 compatibility mode) */
 #define NOC_ROUTE_PMDR   0u /* productive ports x then y; deflect to the first free
                                existing port in N,S,E,W         */
@@ -103,7 +108,10 @@ typedef struct noc_sim_config {
                                   multi-GPU partition on one device); 0/1 = none.
                                   Results are identical for every value.         */
     uint32_t route;            /* NOC_ROUTE_* (0 = the paper's reading)           */
-    uint32_t reserved[6];      /* must be 0                                        */
+    uint32_t dir_mode;         /* NOC_DIR_* (LSPD): where the location array lives */
+    uint32_t dir_node;         /* NOC_DIR_CENTRAL: the node holding the whole
+                                  directory (0..N-1); ignored otherwise          */
+    uint32_t reserved[4];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list

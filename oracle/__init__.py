@@ -57,6 +57,7 @@ class _Config(C.Structure):
         ("l2_hit_lat", C.c_uint32), ("mem_lat", C.c_uint32), ("nfl_ra", C.c_uint32),
         ("sendq_cap", C.c_uint32), ("hist_bins", C.c_uint32), ("seed", C.c_uint64),
         ("script", C.POINTER(_Event)), ("n_script", C.c_uint64), ("route", C.c_uint32),
+        ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
     ]
 
 

@@ -212,6 +212,14 @@ static int l2_hit(orc_sim *s, uint32_t n, uint32_t T)
     return 0;
 }
 
+/* Home node of tag T: the distributed directory (R12, T mod N) or, in the
+ * centralized organisation the paper simulates (NEXT-f3),
+ * the one directory node for every tag (R40). */
+static uint32_t home_of(const orc_sim *s, uint32_t T)
+{
+    return s->cfg.dir_mode ? s->cfg.dir_node : T % s->N;
+}
+
 /* EV handler at home h (R13): the only writer of loc[T] besides DIRSERVICE */
 static void ev_handler(orc_sim *s, uint32_t h, uint32_t T, uint32_t src)
 {
@@ -242,7 +250,7 @@ static void install(orc_sim *s, uint32_t n, uint32_t T)
     }
     if (L[victim].valid) {
         uint32_t V = L[victim].tag;
-        uint32_t hv = V % s->N;
+        uint32_t hv = home_of(s, V);
         s->c.evictions += 1;
         s->c.evs_sent += 1;
         if (hv == n) ev_handler(s, n, V, n);
@@ -326,7 +334,7 @@ static void start_access(orc_sim *s, uint32_t n, uint32_t T)
             c->ready = s->t + s->cfg.l2_hit_lat;
         }
     } else {
-        uint32_t h = T % s->N;             /* home node of T (R12) */
+        uint32_t h = home_of(s, T);        /* home node of T (R12, R40) */
         s->c.l2_misses += 1;
         c->mode = M_WAIT_DIR;
         if (h == n) dir_service(s, n, T, n);
@@ -727,6 +735,10 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         set_err("mesh must be 2..2048 per side and at most 2^21 nodes"); return ORC_EINVAL;
     }
     if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1) { set_err("bad mode/prio/route"); return ORC_EINVAL; }
+    if (cfg->dir_mode > 1 || (cfg->dir_mode && (uint64_t)cfg->dir_node >= (uint64_t)cfg->mesh_w * cfg->mesh_h)) {
+        set_err("bad dir_mode/dir_node");
+        return ORC_EINVAL;
+    }
     if (cfg->sendq_cap == 0 || cfg->sendq_cap > 1024 || (cfg->sendq_cap & (cfg->sendq_cap - 1))) {
         set_err("sendq_cap must be a power of two in 1..1024"); return ORC_EINVAL;
     }

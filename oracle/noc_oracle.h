@@ -64,6 +64,8 @@ typedef struct {
     const orc_event *script;     /* optional, may be NULL                   */
     uint64_t n_script;
     uint32_t route;              /* ORC_ROUTE_*                             */
+    uint32_t dir_mode;           /* 0: home(T) = T mod N (R12); 1: central  */
+    uint32_t dir_node;           /* dir_mode 1: the node holding the directory */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */

@@ -46,7 +46,8 @@ class noc_sim_config(C.Structure):
         ("script", C.POINTER(noc_sim_event)), ("n_script", C.c_uint64),
         ("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("engine", C.c_uint32), ("nccl_id", C.c_uint8 * 128), ("bands", C.c_uint32),
-        ("route", C.c_uint32), ("reserved", C.c_uint32 * 6),
+        ("route", C.c_uint32), ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
+        ("reserved", C.c_uint32 * 4),
     ]
 
 

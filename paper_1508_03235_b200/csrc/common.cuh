@@ -143,6 +143,8 @@ struct Dev {
     // geometry and model parameters
     uint32_t W, H, N, n0, nloc, row0, rows;
     uint32_t mode, prio, route, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
+    uint32_t dir_mode, dir_node;      // NEXT-f3: central directory at dir_node (R40)
+    uint64_t loc_n;                   // directory entries held by this band
     uint32_t qcap, nb, seed_lo, seed_hi;
     uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi
     uint32_t gen;                     // generation enabled (0 during drain)

@@ -279,12 +279,15 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
 __global__ void k_hash_loc(Dev S, unsigned long long *out)
 {
     uint64_t H = 0;
-    const uint64_t total = (uint64_t)S.tpn * S.nloc;
+    const uint64_t total = S.loc_n;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t e = S.loc[i];
         if (!e) continue;
-        uint64_t q = i / S.nloc, lh = i - q * S.nloc;
-        uint64_t T = q * S.N + S.n0 + lh;
+        uint64_t T = i;   // centralized: the entry index is the tag
+        if (!S.dir_mode) {
+            const uint64_t q = i / S.nloc, lh = i - q * S.nloc;
+            T = q * S.N + S.n0 + lh;
+        }
         H += hterm(D_LOC, T, TupleHash(2).add(e & HOLDER_MASK).add(e >> HOLDER_BITS).h);
     }
     __shared__ unsigned long long red[32];

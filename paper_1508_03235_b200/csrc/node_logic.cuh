@@ -83,8 +83,19 @@ __device__ __forceinline__ void enq(const Dev &S, const Sink &K, NodeCtx &c, uin
     K.cnt(S, C_ENQ);
 }
 
+// Home node of tag T: T mod N (distributed, R12), or the one directory node
+// (centralized, the paper's location array; R40)
+__device__ __forceinline__ uint32_t home_of(const Dev &S, uint32_t T)
+{
+    return S.dir_mode ? S.dir_node : T % S.N;
+}
+
+// Entry of tag T in this band's part of the location array (only called at
+// T's home): distributed = [T / N][home - n0]; centralized = [T] in the band of
+// the directory node
 __device__ __forceinline__ size_t loc_index(const Dev &S, uint32_t T)
 {
+    if (S.dir_mode) return T;
     uint32_t q = T / S.N, h = T - q * S.N;
     return (size_t)q * S.nloc + (h - S.n0);
 }
@@ -137,7 +148,7 @@ static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t
     }
     if (vline.x != 0u) {
         uint32_t V = vline.x - 1u;
-        uint32_t hv = V % S.N;
+        uint32_t hv = home_of(S, V);
         K.cnt(S, C_EVICTIONS);
         K.cnt(S, C_EVSENT);
         if (hv == c.n) ev_handler(S, K, V, c.n);
@@ -220,7 +231,7 @@ static __device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uin
     } else {
         K.cnt(S, C_L2MISS);
         set_mode(c, MWAITDIR, 0);
-        uint32_t h = T % S.N;
+        uint32_t h = home_of(S, T);
         if (h == c.n) dir_service(S, K, c, T, c.n, t);
         else enq(S, K, c, KDA, h, T, 1u);
     }

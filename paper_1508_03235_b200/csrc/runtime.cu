@@ -109,6 +109,7 @@ static int validate(const noc_sim_config *c)
     if (c->mesh_w < 2 || c->mesh_h < 2 || c->mesh_w > 2048 || c->mesh_h > 2048 || N > (1u << 21) - 1u)
         return fail(NOC_EINVAL, "mesh must be 2..2048 per side and at most 2^21-1 nodes (R9, R32)");
     if (c->mode > 1 || c->prio > 1 || c->route > 1) return fail(NOC_EINVAL, "mode/prio/route out of range");
+    if (c->dir_mode > 1 || (c->dir_mode && c->dir_node >= N)) return fail(NOC_EINVAL, "dir_mode/dir_node out of range");
     if (c->sendq_cap == 0 || c->sendq_cap > 1024 || (c->sendq_cap & (c->sendq_cap - 1)))
         return fail(NOC_EINVAL, "sendq_cap must be a power of two in 1..1024");
     if (c->hist_bins == 0 || c->hist_bins > 65536) return fail(NOC_EINVAL, "hist_bins must be 1..65536");
@@ -129,7 +130,7 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    for (int i = 0; i < 6; ++i)
+    for (int i = 0; i < 4; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->n_script && !c->script) return fail(NOC_EINVAL, "n_script > 0 with a null script");
     for (uint64_t i = 0; i < c->n_script; ++i) {
@@ -182,6 +183,8 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.mode = cfg->mode;
     D.prio = cfg->prio;
     D.route = cfg->route;
+    D.dir_mode = cfg->mode == NOC_MODE_LSPD ? cfg->dir_mode : 0u;
+    D.dir_node = cfg->dir_node;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
@@ -212,7 +215,11 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
         if ((rc = dalloc(s, &D.core_cold, n))) return rc;
         if ((rc = dalloc(s, &D.l2, n * D.sets * D.ways))) return rc;
         uint64_t b0 = s->bytes;
-        if ((rc = dalloc(s, &D.loc, (size_t)D.tpn * n))) return rc;
+        // distributed: the entries of the tags homed on this band's nodes;
+        // centralized: the whole array in the directory node's band (R40)
+        if (D.dir_mode) D.loc_n = (D.dir_node >= D.n0 && D.dir_node < D.n0 + D.nloc) ? (uint64_t)D.tpn * D.N : 0u;
+        else D.loc_n = (uint64_t)D.tpn * n;
+        if ((rc = dalloc(s, &D.loc, (size_t)D.loc_n))) return rc;
         s->loc_bytes += s->bytes - b0;
     }
     // script events of this band's nodes, per node ordered by (cycle, input order)

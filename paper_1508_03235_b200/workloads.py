@@ -15,6 +15,7 @@ from fractions import Fraction
 MODE_UR, MODE_LSPD = 0, 1
 PRIO_DEFLECT, PRIO_OLDEST = 0, 1
 ROUTE_PMDR, ROUTE_XY = 0, 1   # NEXT-f4: strict XY + N,E,S,W deflection
+DIR_DISTRIBUTED, DIR_CENTRAL = 0, 1   # NEXT-f3: one node holds the whole directory
 
 
 def thr(p) -> int:
@@ -29,7 +30,7 @@ BASE = dict(
     tags_per_node=128, priv_tags=96,
     thr_inj=thr(0.1), thr_priv=thr(0.5),
     l2_hit_lat=1, mem_lat=100, nfl_ra=4,
-    sendq_cap=16, hist_bins=4096, seed=1, route=0,
+    sendq_cap=16, hist_bins=4096, seed=1, route=0, dir_mode=0, dir_node=0,
 )
 
 
@@ -64,8 +65,8 @@ def c1b(seed=1, **kw):
 def lspd(w, h, seed=1, lam=0.05, **kw):
     """LSPD with the Table III rows 3-4 slice (32 sets x 2 ways x 32 B)."""
     kw.setdefault("p_priv", 0.5)
-    return make(mesh_w=w, mesh_h=h, mode=MODE_LSPD, l2_sets=32, l2_ways=2, lam=lam,
-                sendq_cap=32, seed=seed, **kw)
+    kw.setdefault("sendq_cap", 32)
+    return make(mesh_w=w, mesh_h=h, mode=MODE_LSPD, l2_sets=32, l2_ways=2, lam=lam, seed=seed, **kw)
 
 
 def c2(seed=1, **kw):
@@ -115,4 +116,33 @@ def random_script(cfg: dict, n_events: int, max_cycle: int, seed: int):
         else:
             v = rng.randrange(cfg["tags_per_node"] * N)
         ev.append((cyc, node, v))
+    return ev
+
+
+def load_trace(path: str, cfg: dict):
+    """Trace replay input (grammar of SPEC S:L533-534):
+    one record per line, `<node_linear_id> <hex_address> [R|W]`, `#` comments
+    and blank lines ignored.  Each node's records become its address stream in
+    file order: script events (0, node, tag) with tag = (address // line bytes)
+    mod TPN*N (reading R41), consumed one per generation opportunity in place
+    of the Philox draw (DESIGN 3.3; the paper feeds a trace per cycle, P:L233,
+    L276).  R/W is accepted and ignored (the model has no dirty state).
+    Returns the event list; raises ValueError on a malformed line."""
+    N = cfg["mesh_w"] * cfg["mesh_h"]
+    space = cfg["tags_per_node"] * N
+    line_bytes = max(1, int(cfg.get("l2_line_bytes", 32)))
+    ev = []
+    with open(path) as f:
+        for ln, line in enumerate(f, 1):
+            body = line.split("#", 1)[0].strip()
+            if not body:
+                continue
+            tok = body.split()
+            if len(tok) not in (2, 3) or (len(tok) == 3 and tok[2] not in ("R", "W")):
+                raise ValueError("%s:%d: expected '<node> <hex_address> [R|W]'" % (path, ln))
+            node = int(tok[0], 10)
+            addr = int(tok[1], 16)
+            if not 0 <= node < N or addr < 0:
+                raise ValueError("%s:%d: node or address out of range" % (path, ln))
+            ev.append((0, node, (addr // line_bytes) % space))
     return ev

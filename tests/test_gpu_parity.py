@@ -323,3 +323,53 @@ def test_c4_sweep_endpoints(mode, lam):
     engine) bit-exact against the oracle."""
     g, o = both(W.c4(lam, mode=mode), 600)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("cfg", [
+    W.c1b(dir_mode=W.DIR_CENTRAL, dir_node=5, lam=0.05),
+    W.lspd(24, 20, lam=0.02, dir_mode=W.DIR_CENTRAL, dir_node=10 * 24 + 12, sendq_cap=64),
+], ids=["c1b", "lspd24x20"])
+def test_centralized_directory(cfg, engine):
+    """NEXT-f3: the paper's centralized location array (R40)
+    at one node, on every engine, bit-exact against the oracle."""
+    g, o = both(cfg, 4000, engine)
+    assert_same(g, o)
+    st = g.stats()[0]
+    assert st["dir_searches"] > 0 and st["evs_received"] > 0
+    if cfg["mesh_w"] == 4:
+        # 16 cores stay below the directory node's one ejection per cycle; at
+        # 24x20 the closed loop offers ~4 directory accesses per cycle and the
+        # directory node's send FIFO overflows (the hot spot of P:L71, R21
+        # drop counters), identically on both sides
+        assert sum(v for k, v in st.items() if k.startswith("drops_")) == 0
+
+
+def test_centralized_directory_c3_and_bands():
+    """C3 with the directory at the centre node (the hot spot the paper warns
+    about), and the same across 4 virtual bands (the directory band
+    receives every DA over band edges)."""
+    cfg = W.c3(lam=0.002, dir_mode=W.DIR_CENTRAL, dir_node=104 * 208 + 104, sendq_cap=256)
+    g, o = both(cfg, 600)
+    assert_same(g, o)
+    cfg = W.lspd(22, 19, lam=0.02, dir_mode=W.DIR_CENTRAL, dir_node=9 * 22 + 11, sendq_cap=64)
+    for engine in (nb.ENGINE_TILED, nb.ENGINE_PERSIST):
+        g = nb.NocSim(cfg, bands=4, engine=engine)
+        o = Oracle(cfg)
+        g.run(2000)
+        o.run(2000)
+        assert_same(g, o)
+
+
+def test_trace_replay_central_directory():
+    """NEXT-f3 end to end: a trace file (SPEC grammar) replayed with the
+    directory at one node, on every engine, against the oracle."""
+    import os
+    cfg = W.c1b(thr_inj=0, dir_mode=W.DIR_CENTRAL, dir_node=10)
+    ev = W.load_trace(os.path.join(os.path.dirname(__file__), "golden", "trace_4x4.txt"), cfg)
+    rng = random.Random(5)
+    ev += [(rng.randrange(3000), rng.randrange(16), rng.randrange(128 * 16)) for _ in range(400)]
+    for engine in ENGINES:
+        g, o = both(cfg, 5000, engine, script=ev)
+        assert_same(g, o)
+        assert g.stats()[0]["accesses"] == len(ev)

@@ -263,6 +263,9 @@ INV_CFGS = [
     ("ur5x3_xy", W.make(mesh_w=5, mesh_h=3, mode=W.MODE_UR, lam=0.3, route=W.ROUTE_XY)),
     ("lspd6x5_xy", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.2,
                           sendq_cap=32, seed=2, mem_lat=30, route=W.ROUTE_XY)),
+    # NEXT-f3 centralized directory at the centre node (2,2) of a 6x5 mesh
+    ("lspd6x5_central", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.05,
+                               sendq_cap=64, seed=4, mem_lat=30, dir_mode=W.DIR_CENTRAL, dir_node=14)),
 ]
 
 
@@ -481,6 +484,31 @@ def test_fig4_timelines():
             assert st["replies_received"] == 1 and st["requests_made"] == 1
 
 
+def test_fig4_timelines_centralized_directory():
+    """NEXT-f3: with the directory at one node D (R40), every
+    access's directory leg goes to D whatever the tag, against the closed forms
+    of tests/golden/fig4_timelines_central.txt."""
+    for case, S, D, homed, holder, lat in golden("fig4_timelines_central.txt"):
+        S, D, homed = int(S), int(D), int(homed)
+        holder = int(holder) if holder != "-" else None
+        T = tag_homed_at(homed)
+        mem = 100
+        if case == "remote_hit":
+            script, setup = [(0, holder, T), (400, S, T)], [2 * manhattan(holder, D, 4) + 1 + mem]
+        elif case == "trap":
+            script, setup = [(0, holder, T), (20, S, T)], [2 * manhattan(holder, D, 4) + 1 + mem]
+        else:
+            script, setup = [(0, S, T)], []
+        cfg = W.make(mode=W.MODE_LSPD, thr_inj=0, l2_sets=4, l2_ways=2, sendq_cap=32,
+                     dir_mode=W.DIR_CENTRAL, dir_node=D)
+        o = Oracle(cfg, script=script, debug=DBG_INVARIANTS)
+        o.run(1000)
+        st, _, _, ha = o.stats()
+        got = collections.Counter({b: c for b, c in enumerate(ha) if c})
+        assert got == collections.Counter(setup + [int(lat)]), (case, S, D, dict(got))
+        assert st["deflections"] == 0
+
+
 def test_table1_flit_division_of_remote_hit():
     """Table I: DA, DR = 1 flit, remote L2 access RA = 4 flits.  A
     remote hit moves DA + DR + RQ + RA = 1 + 1 + 1 + 4 flits (R18)."""
@@ -524,3 +552,26 @@ def test_miss_under_miss_not_allowed():
         o.run(37)
         st = o.stats()[0]
         assert st["accesses"] - st["completed"] == o.cores_busy() <= 16
+
+
+def test_trace_loader_grammar_and_replay():
+    """NEXT-f3 trace replay input: the SPEC line grammar (comments, blank lines,
+    optional R/W) parses to per-node streams, tag = address // line mod TPN*N
+    (R41); malformed lines are rejected; a replay drains with the Table II
+    equalities and each record starts exactly one access."""
+    cfg = W.c1b(thr_inj=0)
+    ev = W.load_trace(os.path.join(GOLDEN, "trace_4x4.txt"), cfg)
+    assert ev == [(0, 0, 0), (0, 0, 128), (0, 5, 5), (0, 5, 5), (0, 15, 1), (0, 3, 15),
+                  (0, 12, (0x3fffe0 // 32) % (128 * 16))]
+    o = Oracle(cfg, script=ev, debug=DBG_INVARIANTS)
+    o.run(2000)
+    st = o.stats()[0]
+    assert st["accesses"] == len(ev) == st["completed"]
+    assert st["l2_hits"] == 1
+    bad = os.path.join(os.path.dirname(GOLDEN), "_bad_trace.txt")
+    for text in ("0 zz\n", "99 0x10\n", "1 0x10 X\n"):
+        with open(bad, "w") as f:
+            f.write(text)
+        with pytest.raises(ValueError):
+            W.load_trace(bad, cfg)
+    os.unlink(bad)
