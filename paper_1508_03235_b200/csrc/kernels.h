@@ -21,7 +21,7 @@ struct DevSet {
 // (sets S.TX, S.TY) within tiles_budget CTAs; tiled_prepare sets the launch
 // attributes for all bands' tiles in one cooperative launch
 bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np);
-cudaError_t tiled_prepare(uint32_t mode, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
+cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
                           uint32_t *smem_hist);
 cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,
                          uint32_t *activity, cudaStream_t st);

@@ -413,7 +413,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         }
         cudaError_t ce = cudaErrorInvalidConfiguration;
         if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
-                          : tiled_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
+                          : tiled_prepare(cfg->mode, cfg->route, cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {
             s->engine = cand;
             s->t_tpad = np;
