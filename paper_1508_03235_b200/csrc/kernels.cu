@@ -81,7 +81,7 @@ __device__ __forceinline__ void st_release_sys_u32(uint32_t *p, uint32_t v)
 }
 
 template <uint32_t MODE>
-__global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc,
+__global__ void __launch_bounds__(PERSIST_BLOCK, PERSIST_MIN_BLOCKS) k_persist(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc,
                                                          uint32_t pbase, uint32_t smem_hist, uint32_t *activity)
 {
     uint32_t band = 0;
@@ -143,8 +143,20 @@ __global__ void __launch_bounds__(PERSIST_BLOCK) k_persist(const __grid_constant
         __syncthreads();
         if (s_abort) break;
         bool busy = false;
-        for (uint32_t l = lo_node + threadIdx.x; l < hi_node; l += blockDim.x)
+        // the words every node step reads first (occupancy, FIFO control, core
+        // state) are prefetched one node ahead: each thread walks several
+        // nodes per cycle, and at 1M nodes they come from DRAM
+        for (uint32_t l = lo_node + threadIdx.x; l < hi_node; l += blockDim.x) {
+#ifndef NOC_NO_PERSIST_PREFETCH
+            const uint32_t ln = l + blockDim.x;
+            if (ln < hi_node) {
+                prefetch_l1(&S.flag[(uint32_t)t & 1u][ln]);
+                prefetch_l1(&S.fifo_ctl[ln]);
+                if (MODE == 1u) prefetch_l1(&S.core_hot[ln]);
+            }
+#endif
             busy |= node_step_global<MODE>(S, K, l, t, acc);
+        }
         // full BAR.SYNC (see tile_engine.cu); busy nodes stamp a per-parity word
         if (activity && busy) s_busy[c & 1u] = c + 1u;
         __syncthreads();
