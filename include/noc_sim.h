@@ -111,7 +111,11 @@ typedef struct noc_sim_config {
     uint32_t dir_mode;         /* NOC_DIR_* (LSPD): where the location array lives */
     uint32_t dir_node;         /* NOC_DIR_CENTRAL: the node holding the whole
                                   directory (0..N-1); ignored otherwise          */
-    uint32_t reserved[4];      /* must be 0                                        */
+    uint32_t l1_sets;          /* LSPD, NEXT-f1 private write-through L1 (R42):
+                                  0 = none (the base model), else 1..65536      */
+    uint32_t l1_ways;          /* 1..16 (Table III: 32 sets x 2 ways)            */
+    uint32_t l1_miss_lat;      /* "L1 miss cycle" countdown, 1 .. 2^29-1 */
+    uint32_t reserved[1];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list
@@ -124,6 +128,7 @@ typedef struct noc_sim_counters {
     int64_t replies_received, traps_sent, traps_received, mem_requests;
     int64_t installs, evictions, evs_sent, evs_received;
     int64_t drops[8];          /* by kind: PROBE DA DR NDR RQ RA TRAP EV           */
+    int64_t l1_hits, l1_misses, wb_sent, wb_received;   /* NEXT-f1 L1 (R42)       */
 } noc_sim_counters;
 
 /* Runtime facts about a handle (for measurement and the bench). */

@@ -28,6 +28,7 @@ COUNTER_NAMES = (
     "installs", "evictions", "evs_sent", "evs_received",
 )
 KIND_NAMES = ("probe", "da", "dr", "ndr", "rq", "ra", "trap", "ev")
+L1_COUNTER_NAMES = ("l1_hits", "l1_misses", "wb_sent", "wb_received")   # NEXT-f1 (R42)
 
 MODE_UR, MODE_LSPD = 0, 1
 PRIO_DEFLECT, PRIO_OLDEST = 0, 1
@@ -58,12 +59,13 @@ class _Config(C.Structure):
         ("sendq_cap", C.c_uint32), ("hist_bins", C.c_uint32), ("seed", C.c_uint64),
         ("script", C.POINTER(_Event)), ("n_script", C.c_uint64), ("route", C.c_uint32),
         ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
+        ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
     ]
 
 
 class _Counters(C.Structure):
     _fields_ = [("cycle", C.c_int64)] + [(n, C.c_int64) for n in COUNTER_NAMES] + [
-        ("drops", C.c_int64 * 8)]
+        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES]
 
 
 _lib = None
@@ -193,6 +195,8 @@ class Oracle:
             d[n] = getattr(cnt, n)
         for i, k in enumerate(KIND_NAMES):
             d["drops_" + k] = cnt.drops[i]
+        for n in L1_COUNTER_NAMES:
+            d[n] = getattr(cnt, n)
         return d, list(hl), list(hd), list(ha)
 
     def state_hash(self) -> int:

@@ -26,7 +26,7 @@ enum { DIR_N = 0, DIR_S = 1, DIR_E = 2, DIR_W = 3, PORT_EJECT = 4 };
 /* message kinds: Table I + readings R16, R18, R13 */
 enum { K_PROBE = 0, K_DA = 1, K_DR = 2, K_NDR = 3, K_RQ = 4, K_RA = 5, K_TRAP = 6, K_EV = 7 };
 /* core modes ("miss under a miss is not allowed"; DESIGN 3.4) */
-enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4 };
+enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4, M_L1WAIT = 5 };
 
 #define HOLDER_NONE 0xFFFFFFFFu
 #define AGE_MAX     65535u   /* R32: field width of the deflection age */
@@ -47,6 +47,11 @@ typedef struct { int valid; uint32_t tag; uint64_t stamp; } Line;  /* L2 line (P
 
 typedef struct { uint32_t holder; uint32_t pend; } LocEntry;     /* location array */
 
+/* private L1 line (NEXT-f1, R42): the block tag, last touch, and the node
+ * whose L2 slice supplied it (where the victim writeback goes) */
+typedef struct { int valid; uint32_t tag; uint64_t stamp; uint32_t owner; } L1Line;
+#define WB_BIT 0x80000000u   /* an EV flit whose payload carries this bit is an L1 writeback */
+
 typedef struct {
     Flit in[4];        /* Router.Input[4]: flits to be read this cycle        */
     Flit nin[4];       /* inputs of the next cycle, written by neighbours      */
@@ -60,6 +65,7 @@ typedef struct {
     int install;
     uint32_t rx;       /* Core.ReOrderBuffer, reduced to a counter (R20)       */
     Line *l2;          /* Core.L2 LSPDSlice                                    */
+    L1Line *l1;        /* Core.L1 (NEXT-f1), l1_sets x l1_ways                 */
     uint64_t script_pos, script_end;
     uint64_t script_used;
 } Node;
@@ -71,6 +77,7 @@ struct orc_sim {
     Node *nodes;
     Packet *fifo_store;
     Line *l2_store;
+    L1Line *l1_store;
     LocEntry *loc;
     uint64_t ntags;
     orc_event *script;
@@ -262,6 +269,48 @@ static void install(orc_sim *s, uint32_t n, uint32_t T)
     s->c.installs += 1;
 }
 
+/* ------------------------------------------------------------------------
+ * Private write-through L1 (NEXT-f1, reading R42):
+ * same block size as L2 (Table III, 43k config: 32,2,32 / 32,2,32), LRU by
+ * last touch like L2 (R23).  A hit touches the line.
+ * ---------------------------------------------------------------------- */
+static int l1_hit(orc_sim *s, uint32_t n, uint32_t T)
+{
+    uint32_t set = T % s->cfg.l1_sets;
+    L1Line *L = &s->nodes[n].l1[(uint64_t)set * s->cfg.l1_ways];
+    for (uint32_t w = 0; w < s->cfg.l1_ways; ++w)
+        if (L[w].valid && L[w].tag == T) { L[w].stamp = s->t; return 1; }
+    return 0;
+}
+
+/* "A L1 cache block replacement happens when a new block comes in to local
+ * L1 cache either from local L2 cache or from remote L2 cache ... The evicted
+ * block need to be written back to ... corresponding L2 block":
+ * the victim goes back to the slice that supplied it, as a 1-flit writeback
+ * (an EV flit with WB_BIT), or is absorbed locally when that slice is ours. */
+static void l1_fill(orc_sim *s, uint32_t n, uint32_t T, uint32_t owner)
+{
+    if (!s->cfg.l1_sets) return;
+    uint32_t set = T % s->cfg.l1_sets;
+    L1Line *L = &s->nodes[n].l1[(uint64_t)set * s->cfg.l1_ways];
+    uint32_t w, victim = 0;
+    int found_invalid = 0;
+    for (w = 0; w < s->cfg.l1_ways; ++w)
+        if (!L[w].valid) { victim = w; found_invalid = 1; break; }
+    if (!found_invalid)
+        for (w = 1; w < s->cfg.l1_ways; ++w)
+            if (L[w].stamp < L[victim].stamp) victim = w;
+    if (L[victim].valid) {
+        s->c.wb_sent += 1;
+        if (L[victim].owner == n) s->c.wb_received += 1;
+        else enq(s, n, K_EV, L[victim].owner, L[victim].tag | WB_BIT, 1);
+    }
+    L[victim].valid = 1;
+    L[victim].tag = T;
+    L[victim].stamp = s->t;
+    L[victim].owner = owner;
+}
+
 /* An access is complete: record its latency (R31) and free the core */
 static void complete(orc_sim *s, uint32_t n)
 {
@@ -317,17 +366,14 @@ static void dir_service(orc_sim *s, uint32_t h, uint32_t T, uint32_t r)
     }
 }
 
-/* A new access by the core of n to block T (Phase 1; R19) */
-static void start_access(orc_sim *s, uint32_t n, uint32_t T)
+/* The local L2 part of an access (Fig. 4): hit, else the directory */
+static void l2_access(orc_sim *s, uint32_t n, uint32_t T)
 {
     Node *c = &s->nodes[n];
-    c->tag = T;
-    c->start = s->t;
-    c->rx = 0;
-    s->c.accesses += 1;
     if (l2_hit(s, n, T)) {
         s->c.l2_hits += 1;
         if (s->cfg.l2_hit_lat == 0) {
+            l1_fill(s, n, T, n);
             complete(s, n);
         } else {
             c->mode = M_L2WAIT;
@@ -340,6 +386,30 @@ static void start_access(orc_sim *s, uint32_t n, uint32_t T)
         if (h == n) dir_service(s, n, T, n);
         else enq(s, n, K_DA, h, T, 1);
     }
+}
+
+/* A new access by the core of n to block T (Phase 1; R19): the L1
+ * first when there is one (a hit is served at once; a miss waits the L1 miss
+ * cycles before the local L2 is accessed), else the L2 directly */
+static void start_access(orc_sim *s, uint32_t n, uint32_t T)
+{
+    Node *c = &s->nodes[n];
+    c->tag = T;
+    c->start = s->t;
+    c->rx = 0;
+    s->c.accesses += 1;
+    if (s->cfg.l1_sets) {
+        if (l1_hit(s, n, T)) {
+            s->c.l1_hits += 1;
+            complete(s, n);
+            return;
+        }
+        s->c.l1_misses += 1;
+        c->mode = M_L1WAIT;
+        c->ready = s->t + s->cfg.l1_miss_lat;
+        return;
+    }
+    l2_access(s, n, T);
 }
 
 /* Next script event of node n that is due at cycle t, if any. */
@@ -386,9 +456,14 @@ static void phase1(orc_sim *s, uint32_t n)
     }
 
     /* LSPD */
-    if (c->mode == M_L2WAIT && c->ready == s->t) complete(s, n);
+    if (c->mode == M_L1WAIT && c->ready == s->t) l2_access(s, n, c->tag);
+    if (c->mode == M_L2WAIT && c->ready == s->t) {
+        l1_fill(s, n, c->tag, n);
+        complete(s, n);
+    }
     if (c->mode == M_MEMWAIT && c->ready == s->t) {
         if (c->install) install(s, n, c->tag);
+        l1_fill(s, n, c->tag, n);                 /* R42: a memory fill is supplied locally */
         complete(s, n);
     }
     if (c->mode == M_IDLE && s->gen_enabled) {
@@ -636,6 +711,7 @@ static void phase3(orc_sim *s, uint32_t n)
         if (c->rx == s->cfg.nfl_ra) {
             c->rx = 0;
             s->c.replies_received += 1;
+            l1_fill(s, n, c->tag, f.src);         /* supplied by the holder's slice */
             complete(s, n);
         }
         break;
@@ -648,7 +724,8 @@ static void phase3(orc_sim *s, uint32_t n)
         c->ready = s->t + s->cfg.mem_lat;
         break;
     case K_EV:
-        ev_handler(s, n, f.payload, f.src);
+        if (f.payload & WB_BIT) s->c.wb_received += 1;   /* L1 writeback: absorbed (R42) */
+        else ev_handler(s, n, f.payload, f.src);
         break;
     default:
         fail(s, ORC_EASSERT, "unknown flit kind");
@@ -735,6 +812,12 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         set_err("mesh must be 2..2048 per side and at most 2^21 nodes"); return ORC_EINVAL;
     }
     if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1) { set_err("bad mode/prio/route"); return ORC_EINVAL; }
+    if (cfg->mode == ORC_MODE_LSPD && cfg->l1_sets &&
+        (cfg->l1_sets > 65536 || cfg->l1_ways < 1 || cfg->l1_ways > 16 || cfg->l1_miss_lat < 1 ||
+         cfg->l1_miss_lat >= (1u << 29))) {
+        set_err("l1 geometry: sets 0..65536, ways 1..16, miss latency 1..2^29-1");
+        return ORC_EINVAL;
+    }
     if (cfg->dir_mode > 1 || (cfg->dir_mode && (uint64_t)cfg->dir_node >= (uint64_t)cfg->mesh_w * cfg->mesh_h)) {
         set_err("bad dir_mode/dir_node");
         return ORC_EINVAL;
@@ -784,10 +867,15 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         s->ntags = (uint64_t)cfg->tags_per_node * N;
         s->l2_store = calloc(N * lines, sizeof(Line));
         s->loc = malloc(s->ntags * sizeof(LocEntry));
-        bad = !s->l2_store || !s->loc;
+        const uint64_t l1lines = (uint64_t)cfg->l1_sets * cfg->l1_ways;
+        s->l1_store = calloc(N * l1lines + 1, sizeof(L1Line));
+        bad = !s->l2_store || !s->loc || !s->l1_store;
         if (!bad) {
             for (uint64_t T = 0; T < s->ntags; ++T) { s->loc[T].holder = HOLDER_NONE; s->loc[T].pend = 0; }
-            for (uint64_t n = 0; n < N; ++n) s->nodes[n].l2 = &s->l2_store[n * lines];
+            for (uint64_t n = 0; n < N; ++n) {
+                s->nodes[n].l2 = &s->l2_store[n * lines];
+                s->nodes[n].l1 = &s->l1_store[n * l1lines];
+            }
         }
     }
     if (cfg->n_script && !bad) {
@@ -825,7 +913,7 @@ int orc_create(const orc_config *cfg, orc_sim **out)
 void orc_destroy(orc_sim *s)
 {
     if (!s) return;
-    free(s->nodes); free(s->fifo_store); free(s->l2_store); free(s->loc);
+    free(s->nodes); free(s->fifo_store); free(s->l2_store); free(s->l1_store); free(s->loc);
     free(s->script); free(s->hl); free(s->hd); free(s->ha);
     free(s);
 }
@@ -901,7 +989,7 @@ static uint64_t term(uint64_t dom, uint64_t idx, const uint64_t *v, int k)
 }
 
 enum { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, D_LOC = 6,
-       D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10 };
+       D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10, D_L1 = 11 };
 
 uint64_t orc_state_hash(const orc_sim *s)
 {
@@ -928,6 +1016,7 @@ uint64_t orc_state_hash(const orc_sim *s)
             case M_WAIT_DIR:  tag = c->tag; break;
             case M_WAIT_DATA: tag = c->tag; rx = c->rx; break;
             case M_MEMWAIT:   ready = c->ready; tag = c->tag; inst = (uint64_t)c->install; break;
+            case M_L1WAIT:    ready = c->ready; tag = c->tag; break;
             }
             v[0] = (uint64_t)c->mode; v[1] = ready; v[2] = tag; v[3] = inst; v[4] = start; v[5] = rx;
             H += term(D_CORE, n, v, 6);
@@ -940,6 +1029,16 @@ uint64_t orc_state_hash(const orc_sim *s)
                     if (!L->valid) continue;
                     v[0] = L->tag; v[1] = L->stamp;
                     H += term(D_L2, ((uint64_t)n * S + st) * Wy + w, v, 2);
+                }
+        }
+        if (s->cfg.mode == ORC_MODE_LSPD && s->cfg.l1_sets) {
+            uint32_t S = s->cfg.l1_sets, Wy = s->cfg.l1_ways;
+            for (uint32_t st = 0; st < S; ++st)
+                for (uint32_t w = 0; w < Wy; ++w) {
+                    const L1Line *L = &c->l1[(uint64_t)st * Wy + w];
+                    if (!L->valid) continue;
+                    v[0] = L->tag; v[1] = L->stamp; v[2] = L->owner;
+                    H += term(D_L1, ((uint64_t)n * S + st) * Wy + w, v, 3);
                 }
         }
         if (c->script_used) { v[0] = c->script_used; H += term(D_SCRIPT, n, v, 1); }

@@ -66,6 +66,8 @@ typedef struct {
     uint32_t route;              /* ORC_ROUTE_*                             */
     uint32_t dir_mode;           /* 0: home(T) = T mod N (R12); 1: central  */
     uint32_t dir_node;           /* dir_mode 1: the node holding the directory */
+    uint32_t l1_sets, l1_ways;   /* NEXT-f1 private L1 (Table III); 0 sets = none */
+    uint32_t l1_miss_lat;        /* "L1 miss cycle" countdown, >= 1 */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */
@@ -77,6 +79,7 @@ typedef struct {
     int64_t replies_received, traps_sent, traps_received, mem_requests;
     int64_t installs, evictions, evs_sent, evs_received;
     int64_t drops[8];
+    int64_t l1_hits, l1_misses, wb_sent, wb_received;   /* NEXT-f1 (R42) */
 } orc_counters;
 
 typedef struct orc_sim orc_sim;

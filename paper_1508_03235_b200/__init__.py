@@ -26,6 +26,7 @@ COUNTER_NAMES = (
     "installs", "evictions", "evs_sent", "evs_received",
 )
 KIND_NAMES = ("probe", "da", "dr", "ndr", "rq", "ra", "trap", "ev")
+L1_COUNTER_NAMES = ("l1_hits", "l1_misses", "wb_sent", "wb_received")   # NEXT-f1 (R42)
 
 NOC_OK, NOC_EINVAL, NOC_ENOMEM, NOC_ECUDA, NOC_ENCCL, NOC_EOVERFLOW, NOC_ESTATE = 0, -1, -2, -3, -4, -5, -6
 ENGINE_AUTO, ENGINE_STEP, ENGINE_PERSIST, ENGINE_TILED, ENGINE_TILED4 = 0, 1, 2, 3, 4
@@ -47,13 +48,14 @@ class noc_sim_config(C.Structure):
         ("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
         ("engine", C.c_uint32), ("nccl_id", C.c_uint8 * 128), ("bands", C.c_uint32),
         ("route", C.c_uint32), ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
-        ("reserved", C.c_uint32 * 4),
+        ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
+        ("reserved", C.c_uint32 * 1),
     ]
 
 
 class noc_sim_counters(C.Structure):
     _fields_ = [("cycle", C.c_int64)] + [(n, C.c_int64) for n in COUNTER_NAMES] + [
-        ("drops", C.c_int64 * 8)]
+        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES]
 
 
 class noc_sim_info(C.Structure):
@@ -162,6 +164,8 @@ def noc_sim_stats(h, nbins: int):
         d[n] = getattr(cnt, n)
     for i, k in enumerate(KIND_NAMES):
         d["drops_" + k] = cnt.drops[i]
+    for n in L1_COUNTER_NAMES:
+        d[n] = getattr(cnt, n)
     return d, list(hl), list(hd), list(ha)
 
 

@@ -13,13 +13,16 @@ enum : uint32_t { PN = 0, PS = 1, PE = 2, PW = 3, PX = 4 };
 // message kinds (Table I; DESIGN 3.2)
 enum : uint32_t { KPROBE = 0, KDA = 1, KDR = 2, KNDR = 3, KRQ = 4, KRA = 5, KTRAP = 6, KEV = 7 };
 // core modes (DESIGN 3.2)
-enum : uint32_t { MIDLE = 0, ML2WAIT = 1, MWAITDIR = 2, MWAITDATA = 3, MMEMWAIT = 4 };
+enum : uint32_t { MIDLE = 0, ML2WAIT = 1, MWAITDIR = 2, MWAITDATA = 3, MMEMWAIT = 4, ML1WAIT = 5 };
+// an EV flit whose payload carries this bit is an L1 victim writeback (NEXT-f1, R42;
+// tags are < 2^31, R32)
+constexpr uint32_t WB_BIT = 0x80000000u;
 // counter indices (DESIGN 3.6)
 enum : uint32_t {
     C_GENERATED = 0, C_ENQ, C_INJECTED, C_EJECTED, C_HOPS, C_DEFL, C_PROBES, C_ACCESSES,
     C_COMPLETED, C_L2HIT, C_L2MISS, C_DIRSEARCH, C_REQMADE, C_REQRCVD, C_REPSENT, C_REPRCVD,
     C_TRAPSENT, C_TRAPRCVD, C_MEMREQ, C_INSTALLS, C_EVICTIONS, C_EVSENT, C_EVRCVD,
-    C_DROPS = 23, NCOUNTERS = 31
+    C_DROPS = 23, C_L1HIT = 31, C_L1MISS, C_WBSENT, C_WBRCVD, NCOUNTERS = 35
 };
 // error flags
 enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8 };
@@ -132,7 +135,7 @@ __host__ __device__ __forceinline__ uint64_t hterm(uint64_t dom, uint64_t idx, u
 }
 
 enum : uint64_t { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, D_LOC = 6,
-                  D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10 };
+                  D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10, D_L1 = 11 };
 
 // ---------------------------------------------------------------------------
 // Device view of one simulation (passed by value to every kernel).
@@ -144,6 +147,7 @@ struct Dev {
     uint32_t W, H, N, n0, nloc, row0, rows;
     uint32_t mode, prio, route, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
     uint32_t dir_mode, dir_node;      // NEXT-f3: central directory at dir_node (R40)
+    uint32_t l1_sets, l1_ways, l1_miss_lat;   // NEXT-f1 private L1 (R42); 0 sets = none
     uint64_t loc_n;                   // directory entries held by this band
     uint32_t qcap, nb, seed_lo, seed_hi;
     uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi
@@ -157,6 +161,7 @@ struct Dev {
     uint32_t *fifo_ctl;               // [nloc]
     uint2 *fifo_pkt;                  // [nloc][qcap]
     uint4 *l2;                        // [nloc][sets][ways] {tag+1 (0 = invalid), stamp_lo, stamp_hi, 0}
+    uint4 *l1;                        // [nloc][l1_sets][l1_ways] {tag+1, stamp_lo, stamp_hi, owner} (NEXT-f1)
     uint32_t *loc;                    // [tpn][nloc] directory entries of tags homed in this band
     const uint4 *script;              // [n_script] {cycle_lo, cycle_hi, value, 0} grouped by node
     const uint32_t *script_off;       // [nloc+1]

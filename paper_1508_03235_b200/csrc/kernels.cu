@@ -253,6 +253,7 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
                 uint64_t r29 = t + (uint64_t)((hot - (uint32_t)t) & 0x1FFFFFFFu);
                 switch (mode) {
                 case ML2WAIT: ready = r29; break;
+                case ML1WAIT: ready = r29; tag = cold.z; break;
                 case MWAITDIR: tag = cold.z; break;
                 case MWAITDATA: tag = cold.z; rx = cold.w >> 1; break;
                 default: ready = r29; tag = cold.z; inst = cold.w & 1u; break;
@@ -267,6 +268,15 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
                 if (v.x == 0u) continue;
                 uint64_t stamp = ((uint64_t)v.z << 32) | v.y;
                 H += hterm(D_L2, (n * S.sets) * S.ways + i, TupleHash(2).add(v.x - 1u).add(stamp).h);
+            }
+            if (S.l1_sets) {   // NEXT-f1 L1 lines: (tag, stamp, owner)
+                const uint4 *M = S.l1 + (size_t)l * S.l1_sets * S.l1_ways;
+                for (uint32_t i = 0; i < S.l1_sets * S.l1_ways; ++i) {
+                    uint4 v = M[i];
+                    if (v.x == 0u) continue;
+                    uint64_t stamp = ((uint64_t)v.z << 32) | v.y;
+                    H += hterm(D_L1, (n * S.l1_sets) * S.l1_ways + i, TupleHash(3).add(v.x - 1u).add(stamp).add(v.w).h);
+                }
             }
         }
         if (S.has_script) {

@@ -158,6 +158,26 @@ static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t
     K.cnt(S, C_INSTALLS);
 }
 
+// ---------------------------------------------------------------------------
+// Private write-through L1 (NEXT-f1, R42): LRU like L2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool l1_hit(const Dev &S, const NodeCtx &c, uint32_t T, uint64_t t)
+{
+    uint4 *L = S.l1 + ((size_t)c.l * S.l1_sets + T % S.l1_sets) * S.l1_ways;
+    for (uint32_t w = 0; w < S.l1_ways; ++w) {
+        const uint4 v = L[w];
+        if (v.x == T + 1u) {
+            L[w] = make_uint4(v.x, (uint32_t)t, (uint32_t)(t >> 32), v.w);
+            return true;
+        }
+    }
+    return false;
+}
+
+// Fill block T supplied by `owner`'s slice; the victim is written back to the
+// slice that supplied it (1-flit EV with WB_BIT), absorbed when that is ours.
+static __device__ void l1_fill(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t owner, uint64_t t);
+
 __device__ __forceinline__ void complete(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
 {
     load_cold(S, c);
@@ -187,6 +207,31 @@ __device__ __forceinline__ void receive_dr(const Dev &S, const Sink &K, NodeCtx 
     set_mode(c, MWAITDATA, 0);
 }
 
+static __device__ void l1_fill(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t owner, uint64_t t)
+{
+    if (!S.l1_sets) return;
+    uint4 *L = S.l1 + ((size_t)c.l * S.l1_sets + T % S.l1_sets) * S.l1_ways;
+    uint32_t victim = 0;
+    uint64_t best = ~0ull;
+    bool found_invalid = false;
+    uint4 vline = make_uint4(0, 0, 0, 0);
+    for (uint32_t w = 0; w < S.l1_ways; ++w) {
+        const uint4 v = L[w];
+        if (v.x == 0u) {
+            if (!found_invalid) { victim = w; vline = v; found_invalid = true; }
+        } else if (!found_invalid) {
+            const uint64_t st = ((uint64_t)v.z << 32) | v.y;
+            if (st < best) { best = st; victim = w; vline = v; }
+        }
+    }
+    if (vline.x != 0u) {
+        K.cnt(S, C_WBSENT);
+        if (vline.w == c.n) K.cnt(S, C_WBRCVD);
+        else enq(S, K, c, KEV, vline.w, (vline.x - 1u) | WB_BIT, 1u);
+    }
+    L[victim] = make_uint4(T + 1u, (uint32_t)t, (uint32_t)(t >> 32), owner);
+}
+
 // DIRSERVICE at home c.n for requester r (Fig. 4 steps 1-2; R12-R14, R28)
 static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t r, uint64_t t)
 {
@@ -213,18 +258,14 @@ static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint
     }
 }
 
-static __device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+// The local L2 part of an access (Fig. 4): hit, else the directory
+static __device__ void l2_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
 {
-    load_cold(S, c);
-    c.cold = make_uint4((uint32_t)t, (uint32_t)(t >> 32), T, 0u);   // start, tag, install 0, rx 0
-    c.cold_dirty = true;
-    K.cnt(S, C_ACCESSES);
     if (l2_hit(S, c, T, t)) {
         K.cnt(S, C_L2HIT);
         if (S.l2_hit_lat == 0u) {
-            set_mode(c, MIDLE, 0);
-            K.hist(S, 2, 0u);
-            K.cnt(S, C_COMPLETED);
+            l1_fill(S, K, c, T, c.n, t);
+            complete(S, K, c, t);
         } else {
             set_mode(c, ML2WAIT, t + S.l2_hit_lat);
         }
@@ -235,6 +276,27 @@ static __device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uin
         if (h == c.n) dir_service(S, K, c, T, c.n, t);
         else enq(S, K, c, KDA, h, T, 1u);
     }
+}
+
+// A new access (Phase 1; R19): the L1 first when there is one (a hit
+// is served at once; a miss waits the L1 miss cycles, then the local L2)
+static __device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+{
+    load_cold(S, c);
+    c.cold = make_uint4((uint32_t)t, (uint32_t)(t >> 32), T, 0u);   // start, tag, install 0, rx 0
+    c.cold_dirty = true;
+    K.cnt(S, C_ACCESSES);
+    if (S.l1_sets) {
+        if (l1_hit(S, c, T, t)) {
+            K.cnt(S, C_L1HIT);
+            complete(S, K, c, t);
+        } else {
+            K.cnt(S, C_L1MISS);
+            set_mode(c, ML1WAIT, t + S.l1_miss_lat);
+        }
+        return;
+    }
+    l2_access(S, K, c, T, t);
 }
 
 // Next due script event (DESIGN 3.3).  Returns true and the value if one is consumed.
@@ -323,7 +385,7 @@ __device__ __forceinline__ void predraw(const Dev &S, NodeCtx &c, uint64_t t1)
 __device__ __forceinline__ void prefetch_service(const Dev &S, const NodeCtx &c, const Flit &f)
 {
     const uint32_t k = f_kind(f);
-    if (k == KDA || k == KEV) prefetch_l1(&S.loc[loc_index(S, f.w)]);
+    if (k == KDA || (k == KEV && !(f.w & WB_BIT))) prefetch_l1(&S.loc[loc_index(S, f.w)]);
     else if (k == KRQ) prefetch_l1(set_ptr(S, c, f.w));
 }
 
@@ -346,11 +408,15 @@ __device__ __forceinline__ void phase1_ur(const Dev &S, const Sink &K, NodeCtx &
 __device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
 {
     uint32_t mode = core_mode(c.hot);
+    if (mode == ML1WAIT && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {   // NEXT-f1: L1 miss countdown over
+        load_cold(S, c);
+        l2_access(S, K, c, c.cold.z, t);
+        mode = core_mode(c.hot);
+    }
     if ((mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {
-        if (mode == MMEMWAIT) {
-            load_cold(S, c);
-            if (c.cold.w & 1u) install(S, K, c, c.cold.z, t);
-        }
+        load_cold(S, c);
+        if (mode == MMEMWAIT && (c.cold.w & 1u)) install(S, K, c, c.cold.z, t);
+        l1_fill(S, K, c, c.cold.z, c.n, t);       // local L2 hit or memory fill: supplied locally (R42)
         complete(S, K, c, t);
         mode = MIDLE;
     }
@@ -371,15 +437,20 @@ __device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx
 // cycle wbase+k fires (r0 < thr_inj); the value of the window's first firing
 // draw is cached in nd_val.  Outside a window the draw is computed here.  The
 // model is phase1_lspd's; only where the Philox evaluations run differs.
+template <bool L1>
 __device__ __forceinline__ void phase1_lspd_win(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t,
                                                 uint32_t wbase, uint32_t wmask)
 {
     uint32_t mode = core_mode(c.hot);
+    if (L1 && mode == ML1WAIT && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {   // NEXT-f1: L1 miss countdown over
+        load_cold(S, c);
+        l2_access(S, K, c, c.cold.z, t);
+        mode = core_mode(c.hot);
+    }
     if ((mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {
-        if (mode == MMEMWAIT) {
-            load_cold(S, c);
-            if (c.cold.w & 1u) install(S, K, c, c.cold.z, t);
-        }
+        load_cold(S, c);
+        if (mode == MMEMWAIT && (c.cold.w & 1u)) install(S, K, c, c.cold.z, t);
+        if (L1) l1_fill(S, K, c, c.cold.z, c.n, t);   // local L2 hit or memory fill: supplied locally (R42)
         complete(S, K, c, t);
         mode = MIDLE;
     }
@@ -581,6 +652,7 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
             c.cold.w &= 1u;
             c.cold_dirty = true;
             K.cnt(S, C_REPRCVD);
+            l1_fill(S, K, c, c.cold.z, f_src(f), t);   // supplied by the holder's slice (R42)
             complete(S, K, c, t);
         } else {
             c.cold.w = (c.cold.w & 1u) | (rx << 1);
@@ -597,8 +669,9 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
         c.cold_dirty = true;
         set_mode(c, MMEMWAIT, t + S.mem_lat);
         break;
-    default:  // KEV
-        ev_handler(S, K, f.w, f_src(f));
+    default:  // KEV; with WB_BIT an L1 victim writeback, absorbed (R42)
+        if (f.w & WB_BIT) K.cnt(S, C_WBRCVD);
+        else ev_handler(S, K, f.w, f_src(f));
         break;
     }
 }

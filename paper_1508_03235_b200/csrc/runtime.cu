@@ -130,8 +130,10 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    for (int i = 0; i < 4; ++i)
-        if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
+    if (c->reserved[0]) return fail(NOC_EINVAL, "reserved fields must be 0");
+    if (c->mode == NOC_MODE_LSPD && c->l1_sets &&
+        (c->l1_sets > 65536 || c->l1_ways < 1 || c->l1_ways > 16 || c->l1_miss_lat < 1 || c->l1_miss_lat >= (1u << 29)))
+        return fail(NOC_EINVAL, "l1 geometry: sets 0..65536, ways 1..16, miss latency 1..2^29-1");
     if (c->n_script && !c->script) return fail(NOC_EINVAL, "n_script > 0 with a null script");
     for (uint64_t i = 0; i < c->n_script; ++i) {
         const noc_sim_event &e = c->script[i];
@@ -185,6 +187,9 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.route = cfg->route;
     D.dir_mode = cfg->mode == NOC_MODE_LSPD ? cfg->dir_mode : 0u;
     D.dir_node = cfg->dir_node;
+    D.l1_sets = cfg->mode == NOC_MODE_LSPD ? cfg->l1_sets : 0u;
+    D.l1_ways = cfg->l1_ways;
+    D.l1_miss_lat = cfg->l1_miss_lat;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
@@ -214,6 +219,7 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
         if ((rc = dalloc(s, &D.core_hot, n))) return rc;
         if ((rc = dalloc(s, &D.core_cold, n))) return rc;
         if ((rc = dalloc(s, &D.l2, n * D.sets * D.ways))) return rc;
+        if (D.l1_sets && (rc = dalloc(s, &D.l1, n * D.l1_sets * D.l1_ways))) return rc;
         uint64_t b0 = s->bytes;
         // distributed: the entries of the tags homed on this band's nodes;
         // centralized: the whole array in the directory node's band (R40)
@@ -413,7 +419,8 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         }
         cudaError_t ce = cudaErrorInvalidConfiguration;
         if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
-                          : tiled_prepare(cfg->mode, cfg->route, cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
+                          : tiled_prepare(cfg->mode == NOC_MODE_LSPD && cfg->l1_sets ? 2u : cfg->mode, cfg->route,
+                                          cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {
             s->engine = cand;
             s->t_tpad = np;
@@ -663,6 +670,10 @@ extern "C" int noc_sim_stats(noc_sim *s, noc_sim_counters *out, uint64_t *hl, ui
         out->cycle = (int64_t)s->t;
         for (int i = 0; i < NC_NAMED; ++i) dst[i] = (int64_t)c[i];
         for (int k = 0; k < 8; ++k) out->drops[k] = (int64_t)c[C_DROPS + k];
+        out->l1_hits = (int64_t)c[C_L1HIT];
+        out->l1_misses = (int64_t)c[C_L1MISS];
+        out->wb_sent = (int64_t)c[C_WBSENT];
+        out->wb_received = (int64_t)c[C_WBRCVD];
     }
     uint64_t *hs[3] = {hl, hd, ha};
     for (int k = 0; k < 3; ++k)

@@ -269,6 +269,8 @@ constexpr uint32_t NOPORT = 8u;
 
 // ROUTE: the routing mode (R3/R5 PMDR = 0, NEXT-f4 strict XY = 1) as a compile-time
 // parameter: it only shapes the conflict path, which is on every warp's cycle
+// MODE: 0 uniform random, 1 LSPD, 2 LSPD with the NEXT-f1 private L1 (the L1
+// timer checks compiled in only there)
 template <uint32_t MODE, bool DRAIN, uint32_t ROUTE>
 __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
@@ -332,7 +334,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     const uint32_t b0 = (uint32_t)t0 & 1u;
     if (active) {
         c.qctl = S.fifo_ctl[c.l];
-        if (MODE == 1u) {
+        if (MODE != 0u) {
             c.hot = S.core_hot[c.l];
             c.cold = S.core_cold[c.l];
         }
@@ -418,7 +420,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             }
         }
     };
-    const bool windows = MODE == 1u && S.gen && !S.has_script;
+    const bool windows = MODE != 0u && S.gen && !S.has_script;
     if (windows) {
         const uint32_t mode = core_mode(c.hot);
         const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t0) & 0x1FFFFFFFu) == 0u);
@@ -458,7 +460,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             if (has_pend) { phase3(S, K, c, pend, t - 1, acc); has_pend = false; }
             TRACE_P1_BEGIN
             if (MODE == 0u) phase1_ur(S, K, c, t);
-            else phase1_lspd_win(S, K, c, t, wbase, wmask);
+            else phase1_lspd_win<MODE == 2u>(S, K, c, t, wbase, wmask);
             TRACE_P1_END
 
             // (2) latch.  Slots 0..3 = link inputs N,S,E,W,
@@ -667,7 +669,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 // while draining, quiescence is judged at the end of each
                 // cycle, so the service is not deferred there
                 if (DRAIN) phase3(S, K, c, g, t, acc);
-                else { pend = g; has_pend = true; if (MODE == 1u) prefetch_service(S, c, g); }
+                else { pend = g; has_pend = true; if (MODE != 0u) prefetch_service(S, c, g); }
             }
             if (DRAIN) busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
@@ -701,7 +703,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         if (has_pend) phase3(S, K, c, pend, tend - 1, acc);
         if (errf) atomicOr(S.err, errf);
         S.fifo_ctl[c.l] = c.qctl;
-        if (MODE == 1u) {
+        if (MODE != 0u) {
             S.core_hot[c.l] = c.hot;
             S.core_cold[c.l] = c.cold;
         }
@@ -798,13 +800,14 @@ bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
 
 // Shared-memory attribute and co-residency check for one launch of
 // total_tiles CTAs of np threads.
+// kernel mode: 0 UR, 1 LSPD, 2 LSPD with the private L1
 static const void *tiled_fn(uint32_t mode, bool drain, uint32_t route)
 {
-    if (route == 1u)
-        return mode == 1u ? (drain ? (const void *)k_tiled<1, true, 1> : (const void *)k_tiled<1, false, 1>)
-                          : (drain ? (const void *)k_tiled<0, true, 1> : (const void *)k_tiled<0, false, 1>);
-    return mode == 1u ? (drain ? (const void *)k_tiled<1, true, 0> : (const void *)k_tiled<1, false, 0>)
-                      : (drain ? (const void *)k_tiled<0, true, 0> : (const void *)k_tiled<0, false, 0>);
+#define NOC_TF(M)                                                                                       \
+    (route == 1u ? (drain ? (const void *)k_tiled<M, true, 1> : (const void *)k_tiled<M, false, 1>)      \
+                 : (drain ? (const void *)k_tiled<M, true, 0> : (const void *)k_tiled<M, false, 0>))
+    return mode == 2u ? NOC_TF(2) : mode == 1u ? NOC_TF(1) : NOC_TF(0);
+#undef NOC_TF
 }
 
 cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
@@ -850,7 +853,7 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     size_t smem = tiled_smem_bytes(P.d[0], tpad, smem_hist != 0);
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
     const bool dr = activity != nullptr;
-    const void *fn = tiled_fn(P.d[0].mode, dr, P.d[0].route);
+    const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr, P.d[0].route);
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }
 

@@ -373,3 +373,33 @@ def test_trace_replay_central_directory():
         g, o = both(cfg, 5000, engine, script=ev)
         assert_same(g, o)
         assert g.stats()[0]["accesses"] == len(ev)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("cfg", [
+    W.c1b(l1_sets=2, l1_ways=2, l1_miss_lat=3, seed=3),
+    W.lspd(24, 20, lam=0.2, l1_sets=4, l1_ways=2, l1_miss_lat=2),
+    W.lspd(16, 16, lam=0.3, l1_sets=1, l1_ways=1, l1_miss_lat=1, l2_hit_lat=0, dir_mode=W.DIR_CENTRAL,
+           dir_node=8 * 16 + 8, sendq_cap=128),
+], ids=["c1b", "lspd24x20", "lspd16_direct_central"])
+def test_private_l1(cfg, engine):
+    """NEXT-f1: private write-through L1 with the miss countdown and victim
+    writebacks (R42) on every engine, bit-exact against
+    the oracle, then drained (every writeback delivered)."""
+    g, o = both(cfg, 3000, engine, drain=200000)
+    assert_same(g, o)
+    st = g.stats()[0]
+    assert st["l1_hits"] > 0 and st["l1_misses"] > 0 and st["wb_sent"] > 0
+    assert st["wb_sent"] == st["wb_received"]
+
+
+def test_private_l1_c3_table3_geometry():
+    """C3 with Table III's 43k-core L1 (32 sets x 2 ways)."""
+    cfg = W.c3(l1_sets=32, l1_ways=2, l1_miss_lat=2)
+    g, o = both(cfg, 800)
+    assert_same(g, o)
+    g = nb.NocSim(W.lspd(22, 19, lam=0.3, l1_sets=2, l1_ways=2), bands=3)
+    o = Oracle(W.lspd(22, 19, lam=0.3, l1_sets=2, l1_ways=2))
+    g.run(1500)
+    o.run(1500)
+    assert_same(g, o)

@@ -263,6 +263,9 @@ INV_CFGS = [
     ("ur5x3_xy", W.make(mesh_w=5, mesh_h=3, mode=W.MODE_UR, lam=0.3, route=W.ROUTE_XY)),
     ("lspd6x5_xy", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.2,
                           sendq_cap=32, seed=2, mem_lat=30, route=W.ROUTE_XY)),
+    # NEXT-f1 private L1 (Table III 32,2,32 scaled down) in front of the slices
+    ("lspd6x5_l1", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.2,
+                          sendq_cap=32, seed=5, mem_lat=30, l1_sets=2, l1_ways=2, l1_miss_lat=3)),
     # NEXT-f3 centralized directory at the centre node (2,2) of a 6x5 mesh
     ("lspd6x5_central", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.05,
                                sendq_cap=64, seed=4, mem_lat=30, dir_mode=W.DIR_CENTRAL, dir_node=14)),
@@ -575,3 +578,51 @@ def test_trace_loader_grammar_and_replay():
         with pytest.raises(ValueError):
             W.load_trace(bad, cfg)
     os.unlink(bad)
+
+
+def test_l1_timelines_and_writebacks():
+    """NEXT-f1 private L1 (R42) against the closed forms of
+    tests/golden/l1_timelines.txt: an L1 hit is served at once, a miss waits
+    l1_miss_lat before the local L2 / Fig. 4 sequence, and every L1 victim is
+    written back to the slice that supplied it."""
+    for case, S, accs, lats, wbs in golden("l1_timelines.txt"):
+        S = int(S)
+        script, want = [], []
+        cyc = 0
+        holders = []
+        for a in accs.split():
+            if a.startswith("r"):        # remote block: first fetched by its holder
+                holder, home = (int(v) for v in a[1:].split("@"))
+                T = tag_homed_at(home, k=9)
+                if holder not in holders:
+                    script.append((cyc, holder, T))
+                    want.append(2 * manhattan(holder, home, 4) + 1 + 100 + 2)
+                    holders.append(holder)
+                    cyc += 300
+                script.append((cyc, S, T))
+            else:
+                script.append((cyc, S, tag_homed_at(int(a))))
+            cyc += 300
+        want += [int(v) for v in lats.split()]
+        cfg = W.make(mode=W.MODE_LSPD, thr_inj=0, l2_sets=4, l2_ways=2, sendq_cap=32,
+                     l1_sets=1, l1_ways=1, l1_miss_lat=2)
+        o = Oracle(cfg, script=script, debug=DBG_INVARIANTS)
+        o.run(cyc + 300)
+        st, _, _, ha = o.stats()
+        got = collections.Counter({b: c for b, c in enumerate(ha) if c})
+        assert got == collections.Counter(want), (case, dict(got), want)
+        sent, local = (int(v) for v in wbs.split())
+        assert st["deflections"] == 0
+        assert st["wb_sent"] == st["wb_received"] == sent, case
+        assert st["l1_hits"] + st["l1_misses"] == st["accesses"]
+
+
+def test_l1_off_is_the_base_model():
+    """l1_sets = 0 leaves every counter, histogram and the hash of the base
+    model unchanged whatever the other L1 knobs say."""
+    a = Oracle(W.c1b(seed=2))
+    b = Oracle(W.c1b(seed=2, l1_ways=4, l1_miss_lat=7))
+    a.run(3000)
+    b.run(3000)
+    assert a.stats() == b.stats() and a.state_hash() == b.state_hash()
+    assert a.stats()[0]["l1_hits"] == a.stats()[0]["l1_misses"] == 0
