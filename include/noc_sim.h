@@ -115,7 +115,11 @@ typedef struct noc_sim_config {
                                   0 = none (the base model), else 1..65536      */
     uint32_t l1_ways;          /* 1..16 (Table III: 32 sets x 2 ways)            */
     uint32_t l1_miss_lat;      /* "L1 miss cycle" countdown, 1 .. 2^29-1 */
-    uint32_t reserved[1];      /* must be 0                                        */
+    uint32_t inject_mode;      /* 0: R7 (inject only into a free input port);
+                                  1: NEXT-f4, a flit that will eject frees its
+                                  input port for the same cycle.
+                                  Not supported by NOC_ENGINE_TILED4          */
+    uint32_t reserved[4];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list

@@ -60,6 +60,7 @@ class _Config(C.Structure):
         ("script", C.POINTER(_Event)), ("n_script", C.c_uint64), ("route", C.c_uint32),
         ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
+        ("inject_mode", C.c_uint32),
     ]
 
 

@@ -512,7 +512,11 @@ static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t
     int eject_taken = 0;
     uint32_t x = n % W, y = n / W;
 
-    if ((int)nf > degree(W, H, n)) return -1;
+    /* at most one flit per existing port, plus one if a flit ejects (R7; the
+     * NEXT-f4 injection mode can fill a router to degree + 1) */
+    int at_dst = 0;
+    for (uint32_t i = 0; i < nf; ++i) at_dst |= F[i].dst == n;
+    if ((int)nf > degree(W, H, n) + at_dst) return -1;
     /* ranking component: "Priority Sort", insertion sort */
     for (uint32_t i = 0; i < nf; ++i) {
         uint32_t j = i;
@@ -603,8 +607,12 @@ static void phase2(orc_sim *s, uint32_t n)
         }
     }
     /* injection: one flit per cycle through InFromProc, only if a free input
-     * port exists (R7, R8) */
-    if ((int)nf < deg && c->count > 0) {
+     * port exists (R7, R8); under the NEXT-f4 mode (R43) a flit
+     * that will eject frees its input port for the same cycle */
+    int frees = 0;
+    if (s->cfg.inject_mode)
+        for (uint32_t i = 0; i < nf; ++i) frees |= F[i].dst == n;
+    if ((int)nf - frees < deg && c->count > 0) {
         Packet *p = &c->fifo[c->head];
         Flit f;
         f.present = 1;
@@ -811,7 +819,10 @@ int orc_create(const orc_config *cfg, orc_sim **out)
     if (W < 2 || H < 2 || W > 2048 || H > 2048 || (uint64_t)W * H > (1u << 21)) {
         set_err("mesh must be 2..2048 per side and at most 2^21 nodes"); return ORC_EINVAL;
     }
-    if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1) { set_err("bad mode/prio/route"); return ORC_EINVAL; }
+    if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1 || cfg->inject_mode > 1) {
+        set_err("bad mode/prio/route/inject_mode");
+        return ORC_EINVAL;
+    }
     if (cfg->mode == ORC_MODE_LSPD && cfg->l1_sets &&
         (cfg->l1_sets > 65536 || cfg->l1_ways < 1 || cfg->l1_ways > 16 || cfg->l1_miss_lat < 1 ||
          cfg->l1_miss_lat >= (1u << 29))) {

@@ -68,6 +68,7 @@ typedef struct {
     uint32_t dir_node;           /* dir_mode 1: the node holding the directory */
     uint32_t l1_sets, l1_ways;   /* NEXT-f1 private L1 (Table III); 0 sets = none */
     uint32_t l1_miss_lat;        /* "L1 miss cycle" countdown, >= 1 */
+    uint32_t inject_mode;        /* 0: R7; 1: an ejecting flit frees its slot (NEXT-f4) */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */

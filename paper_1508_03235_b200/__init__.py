@@ -49,7 +49,7 @@ class noc_sim_config(C.Structure):
         ("engine", C.c_uint32), ("nccl_id", C.c_uint8 * 128), ("bands", C.c_uint32),
         ("route", C.c_uint32), ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
-        ("reserved", C.c_uint32 * 1),
+        ("inject_mode", C.c_uint32), ("reserved", C.c_uint32 * 4),
     ]
 
 

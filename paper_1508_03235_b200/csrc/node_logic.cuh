@@ -680,11 +680,13 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
 // Injection (R7, R8): one flit of the head packet per cycle, only
 // if fewer flits than ports arrived.  The injected flit takes slot 4.  When the
 // head packet is popped, the next head is fetched (used at t+1 at the earliest).
+// frees: 1 if, under the NEXT-f4 injection mode (R43), a present flit will
+// eject and so frees its input port for this cycle's injection
 __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t npresent, uint64_t t, Acc &acc,
-                                            Flit &out)
+                                            Flit &out, uint32_t frees = 0u)
 {
     const uint32_t qn = q_count(c.qctl);
-    if (qn == 0u || npresent >= c.deg) return false;
+    if (qn == 0u || npresent - frees >= c.deg) return false;
     const uint32_t h = q_head(c.qctl);
     uint32_t nx = q_next(c.qctl);
     if (!c.head_ok) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h]; c.head_ok = true; }
@@ -707,7 +709,11 @@ __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t n
 
 __device__ __forceinline__ void inject(const Dev &S, NodeCtx &c, Inputs &in, uint64_t t, Acc &acc)
 {
-    if (inject_flit(S, c, (uint32_t)__popc(in.present), t, acc, in.f[4])) in.present |= 16u;
+    uint32_t frees = 0u;
+    if (S.inject_mode)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) frees |= ((in.present >> k) & 1u) && f_dst(in.f[k]) == c.n;
+    if (inject_flit(S, c, (uint32_t)__popc(in.present), t, acc, in.f[4], frees)) in.present |= 16u;
 }
 
 // The whole node step of cycle t with links in global memory (SoA).

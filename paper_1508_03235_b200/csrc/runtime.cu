@@ -130,7 +130,11 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    if (c->reserved[0]) return fail(NOC_EINVAL, "reserved fields must be 0");
+    for (int i = 0; i < 4; ++i)
+        if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
+    if (c->inject_mode > 1) return fail(NOC_EINVAL, "inject_mode out of range");
+    if (c->inject_mode && c->engine == NOC_ENGINE_TILED4)
+        return fail(NOC_EINVAL, "inject_mode 1 needs five flit lanes per router: not with the TILED4 engine");
     if (c->mode == NOC_MODE_LSPD && c->l1_sets &&
         (c->l1_sets > 65536 || c->l1_ways < 1 || c->l1_ways > 16 || c->l1_miss_lat < 1 || c->l1_miss_lat >= (1u << 29)))
         return fail(NOC_EINVAL, "l1 geometry: sets 0..65536, ways 1..16, miss latency 1..2^29-1");
@@ -190,6 +194,7 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.l1_sets = cfg->mode == NOC_MODE_LSPD ? cfg->l1_sets : 0u;
     D.l1_ways = cfg->l1_ways;
     D.l1_miss_lat = cfg->l1_miss_lat;
+    D.inject_mode = cfg->inject_mode;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
@@ -403,6 +408,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     // (DESIGN 6.4, profiles/r01_ab_engines.txt)
     for (uint32_t cand : {NOC_ENGINE_TILED, NOC_ENGINE_TILED4}) {
         if (!(s->engine == NOC_ENGINE_AUTO || s->engine == cand)) continue;
+        if (cand == NOC_ENGINE_TILED4 && cfg->inject_mode) continue;   // four lanes per router (R43)
         const bool four = cand == NOC_ENGINE_TILED4;
         bool ok = true;
         uint32_t np = four ? 8 : 32, total = 0;
@@ -419,7 +425,8 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         }
         cudaError_t ce = cudaErrorInvalidConfiguration;
         if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
-                          : tiled_prepare(cfg->mode == NOC_MODE_LSPD && cfg->l1_sets ? 2u : cfg->mode, cfg->route,
+                          : tiled_prepare(cfg->mode == NOC_MODE_LSPD && cfg->l1_sets ? 2u : cfg->mode,
+                                          cfg->route | (cfg->inject_mode << 1),
                                           cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {
             s->engine = cand;

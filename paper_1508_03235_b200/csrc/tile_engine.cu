@@ -267,11 +267,12 @@ struct ExtIn {
 };
 constexpr uint32_t NOPORT = 8u;
 
-// ROUTE: the routing mode (R3/R5 PMDR = 0, NEXT-f4 strict XY = 1) as a compile-time
-// parameter: it only shapes the conflict path, which is on every warp's cycle
+// FEAT: the NEXT-f4 variants as compile-time bits (bit 0: strict-XY routing, R39;
+// bit 1: an ejecting flit frees its port for injection, R43): a runtime check on
+// these per-cycle paths measurably cost 1.5-5 % at C3 (profiles/r01_ab_engines.txt)
 // MODE: 0 uniform random, 1 LSPD, 2 LSPD with the NEXT-f1 private L1 (the L1
 // timer checks compiled in only there)
-template <uint32_t MODE, bool DRAIN, uint32_t ROUTE>
+template <uint32_t MODE, bool DRAIN, uint32_t FEAT>
 __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
 {
@@ -534,7 +535,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             for (uint32_t d = 0; d < 5; ++d) f[d] = Flit{0, 0, 0, 0};
 #pragma unroll
             for (uint32_t d = 0; d < 4; ++d) lds128_if((present >> d) & 1u, fw + d * 16u * np, f[d]);
-            if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4])) present |= 16u;
+            uint32_t frees = 0u;   // NEXT-f4 injection mode (R43): an ejecting flit frees its port
+            if (FEAT & 2u)
+#pragma unroll
+                for (uint32_t d = 0; d < 4; ++d) frees |= ((present >> d) & 1u) && f_dst(f[d]) == c.n;
+            if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4], frees)) present |= 16u;
             TRACE_EV(((present & 16u) ? 32u : 0u) | (present ? 64u : 0u) | (ext ? 128u : 0u));
 
             // (3) first choices (eject at the destination, else x-port, else
@@ -576,7 +581,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     const uint32_t xp = dx > c.x ? PE : PW, yp = dy > c.y ? PS : PN;
                     const uint32_t pw = dst == c.n ? 1u
                                                    : ((dx != c.x ? 2u | (xp << 2) : 0u) |
-                                                      (dy != c.y && (ROUTE == 0u || dx == c.x) ? 16u | (yp << 5) : 0u));
+                                                      (dy != c.y && ((FEAT & 1u) == 0u || dx == c.x) ? 16u | (yp << 5) : 0u));
                     prefs |= (uint64_t)pw << (8u * k);
                     if (k < 4) {
                         const uint32_t life = st - f[k].z;
@@ -614,7 +619,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     } else {
                         if ((pw & 2u) && !((used >> xp) & 1u)) p = xp;
                         else if ((pw & 16u) && !((used >> yp) & 1u)) p = yp;
-                        else { p = defl_port(exist & ~used, ROUTE); dm |= 1u << k; }
+                        else { p = defl_port(exist & ~used, FEAT & 1u); dm |= 1u << k; }
                         used |= 1u << p;
                     }
                     ports |= p << (4u * k);
@@ -800,14 +805,14 @@ bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
 
 // Shared-memory attribute and co-residency check for one launch of
 // total_tiles CTAs of np threads.
-// kernel mode: 0 UR, 1 LSPD, 2 LSPD with the private L1
-static const void *tiled_fn(uint32_t mode, bool drain, uint32_t route)
+// kernel mode: 0 UR, 1 LSPD, 2 LSPD with the private L1; feat: FEAT bits
+static const void *tiled_fn(uint32_t mode, bool drain, uint32_t feat)
 {
-#define NOC_TF(M)                                                                                       \
-    (route == 1u ? (drain ? (const void *)k_tiled<M, true, 1> : (const void *)k_tiled<M, false, 1>)      \
-                 : (drain ? (const void *)k_tiled<M, true, 0> : (const void *)k_tiled<M, false, 0>))
+#define NOC_TD(M, F) (drain ? (const void *)k_tiled<M, true, F> : (const void *)k_tiled<M, false, F>)
+#define NOC_TF(M) (feat == 3u ? NOC_TD(M, 3) : feat == 2u ? NOC_TD(M, 2) : feat == 1u ? NOC_TD(M, 1) : NOC_TD(M, 0))
     return mode == 2u ? NOC_TF(2) : mode == 1u ? NOC_TF(1) : NOC_TF(0);
 #undef NOC_TF
+#undef NOC_TD
 }
 
 cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
@@ -853,7 +858,8 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     size_t smem = tiled_smem_bytes(P.d[0], tpad, smem_hist != 0);
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
     const bool dr = activity != nullptr;
-    const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr, P.d[0].route);
+    const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr,
+                              P.d[0].route | (P.d[0].inject_mode << 1));
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }
 

@@ -403,3 +403,23 @@ def test_private_l1_c3_table3_geometry():
     g.run(1500)
     o.run(1500)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", [nb.ENGINE_STEP, nb.ENGINE_PERSIST, nb.ENGINE_TILED])
+@pytest.mark.parametrize("cfg", [
+    W.make(mesh_w=16, mesh_h=16, mode=W.MODE_UR, lam=0.4, inject_mode=1),
+    W.lspd(24, 20, lam=0.3, inject_mode=1, l1_sets=2, l1_ways=2),
+    W.c1b(inject_mode=1, route=W.ROUTE_XY),
+], ids=["ur16_sat", "lspd24x20_l1", "c1b_xy"])
+def test_inject_when_eject_frees_a_slot_gpu(cfg, engine):
+    """NEXT-f4 injection mode (R43) on the engines with five flit lanes per
+    router, bit-exact against the oracle."""
+    g, o = both(cfg, 3000, engine)
+    assert_same(g, o)
+
+
+def test_inject_mode_c3_and_tiled4_rejected():
+    g, o = both(W.c3(inject_mode=1), 600)
+    assert_same(g, o)
+    with pytest.raises(nb.NocSimError):
+        nb.NocSim(W.c1b(inject_mode=1), engine=nb.ENGINE_TILED4)

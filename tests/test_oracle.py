@@ -626,3 +626,53 @@ def test_l1_off_is_the_base_model():
     b.run(3000)
     assert a.stats() == b.stats() and a.state_hash() == b.state_hash()
     assert a.stats()[0]["l1_hits"] == a.stats()[0]["l1_misses"] == 0
+
+
+@pytest.mark.parametrize("mode,injected", [(0, 2), (1, 3)])
+def test_inject_when_eject_frees_a_slot(mode, injected):
+    """NEXT-f4 injection mode (R43).  2x2 mesh, cycle 0: node 1
+    sends a probe to node 2 (XY: through node 0) and node 2 one to node 0; at
+    cycle 1 both sit at node 0 (degree 2), one of them ejecting, while node 0
+    queues a probe to node 3.  Under R7 node 0 cannot inject at cycle 1 (two
+    flits = degree); when an ejecting flit frees its port it can."""
+    cfg = W.make(mesh_w=2, mesh_h=2, mode=W.MODE_UR, thr_inj=0, inject_mode=mode)
+    o = Oracle(cfg, script=[(0, 1, 2), (0, 2, 0), (1, 0, 3)], debug=DBG_INVARIANTS)
+    o.run(2)
+    assert o.stats()[0]["injected"] == injected
+    o.run(20)
+    st = o.stats()[0]
+    assert st["injected"] == st["ejected"] == 3 and st["deflections"] == 0
+
+
+def test_arbitration_degree_plus_one_with_an_ejecting_flit():
+    """Under the NEXT-f4 injection mode a router holds up to degree + 1 flits
+    when one ejects: the greedy still equals the brute force and never drops a
+    flit (random degree-2/3/4 cases of a 3x3 mesh, both routings)."""
+    rng = random.Random(77)
+    w = h = 3
+    for node in (0, 1, 4):
+        deg = sum(exists(w, h, node, p) for p in range(4))
+        for route in (W.ROUTE_PMDR, W.ROUTE_XY):
+            for _ in range(3000):
+                pool = rng.sample(range(20), 6)
+                flits = [random_flit(rng, 9, pool) for _ in range(deg)]
+                k = rng.randrange(deg)
+                flits[k] = (node,) + flits[k][1:]                 # one of them at its destination
+                flits.append((rng.choice([d for d in range(9) if d != node]), node, 0, 2))   # injected
+                check_case(w, h, node, W.PRIO_DEFLECT, flits, route)
+
+
+@pytest.mark.parametrize("name,cfg", [
+    ("ur6x5_inj", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_UR, lam=0.4, inject_mode=1)),
+    ("lspd6x5_inj", W.make(mesh_w=6, mesh_h=5, mode=W.MODE_LSPD, l2_sets=4, l2_ways=2, lam=0.2,
+                           sendq_cap=32, seed=7, mem_lat=30, inject_mode=1)),
+])
+def test_inject_mode_invariants_and_drain(name, cfg):
+    """Conservation / exclusivity / top-priority progress every cycle and
+    delivery of everything under the NEXT-f4 injection mode."""
+    o = Oracle(cfg, debug=DBG_INVARIANTS)
+    o.run(3000)
+    used, drained = o.drain(200000)
+    assert drained
+    st = o.stats()[0]
+    assert st["injected"] == st["ejected"]
