@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define NOC_SIM_ABI_VERSION 1u
+#define NOC_SIM_ABI_VERSION 2u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters */
 
 /* error codes */
 #define NOC_OK          0

@@ -96,7 +96,7 @@ def lib():
         L.noc_sim_destroy.argtypes = [P]
         L.noc_sim_last_error.restype = C.c_char_p
         L.noc_sim_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
-        if L.noc_sim_abi_version() != 1:
+        if L.noc_sim_abi_version() != 2:   # include/noc_sim.h NOC_SIM_ABI_VERSION
             raise NocSimError(NOC_EINVAL, "ABI version mismatch")
         _lib = L
     return _lib
