@@ -231,11 +231,13 @@ def run_ours(args):
     gpu_launches = launches * (2 if info1["engine"] in (3, 4) else 1)
     per_launch_ms = dev_ms / max(launches, 1)
     achieved = B * nodecycles / (dev_ms / 1e3) / 1e9
-    traffic = None
+    traffic, ncu_info = None, None
     tf = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.workload)
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            tj = json.load(open(tf))
+            traffic = tj.get("dram_bytes_per_launch")
+            ncu_info = {k: tj.get(k) for k in ("dram_bytes_per_node_cycle", "lts_bytes_per_node_cycle", "summary")}
         except Exception:
             traffic = None
 
@@ -271,7 +273,13 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": KERNELS.get(info1["engine"], "engine %d" % info1["engine"]),
-                     "bytes_per_node_cycle": B, "rates": rates, "per_launch_ms": per_launch_ms},
+                     "bytes_per_node_cycle": B, "rates": rates, "per_launch_ms": per_launch_ms,
+                     # the dense accounting (every link slot read and written,
+                     # 32 B of core state) for transparency, and the ncu measurements of the
+                     # same launch (profiles/traffic_<workload>.json) when present
+                     "dense": {"bytes_per_node_cycle": 168.0,
+                               "frac": 168.0 * nodecycles / (dev_ms / 1e3) / 1e9 / peak},
+                     "ncu": ncu_info},
         "clocks": ck,
         "sim": {"hash": None, "drops": sum(v for k, v in delta.items() if k.startswith("drops_"))},
     }
