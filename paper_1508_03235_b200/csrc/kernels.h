@@ -8,7 +8,7 @@ constexpr uint32_t PERSIST_BLOCK = 256;
 // 3 co-resident PERSIST CTAs per SM (<= 80 registers): large meshes are DRAM-latency
 // bound and need the warps (A/B at C5: 24 vs 16 warps per SM, -18% per cycle)
 constexpr uint32_t PERSIST_MIN_BLOCKS = 3;
-constexpr uint32_t TILE_BLOCK_MAX = 512;                  // nodes (= threads) per CTA
+constexpr uint32_t TILE_BLOCK_MAX = 320;                  // nodes (= threads) per CTA: C3 tiles are 300; 320 leaves 204 registers (A/B: -2.7 % per cycle vs 512)
 constexpr uint32_t TILE_MIN_BLOCKS = 1;                   // co-resident CTAs per SM
 
 // Row bands handled by one process (virtual bands on one GPU, or the single
