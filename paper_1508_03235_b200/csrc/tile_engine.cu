@@ -23,6 +23,7 @@
 #include "node_logic.cuh"
 #include "kernels.h"
 #include <cstdio>
+#include <cstdlib>
 
 namespace noc {
 
@@ -793,6 +794,16 @@ bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
             uint64_t tw = (S.W + tx - 1) / tx, th = (S.rows + ty - 1) / ty;
             uint64_t tn = tw * th, per = tw + th;
             if (tn < best_tn || (tn == best_tn && per < best_per)) { best_tn = tn; best_per = per; bx = tx; by = ty; }
+        }
+    }
+    // experiment hook: NOCSIM_TILING=TXxTY forces the tiling when it fits
+    if (const char *e = getenv("NOCSIM_TILING")) {
+        unsigned ex = 0, ey = 0;
+        if (sscanf(e, "%ux%u", &ex, &ey) == 2 && ex >= 1 && ey >= 1 && ex <= S.W && ey <= S.rows &&
+            (uint64_t)ex * ey <= tiles_budget) {
+            bx = ex;
+            by = ey;
+            best_tn = (uint64_t)((S.W + bx - 1) / bx) * ((S.rows + by - 1) / by);
         }
     }
     if (bx == 0 || best_tn > TILE_BLOCK_MAX) return false;
