@@ -27,13 +27,6 @@
 
 namespace noc {
 
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v)
 {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -109,13 +102,6 @@ __device__ __forceinline__ uint32_t tile_slot(const TileShape &T, uint32_t lx, u
     if (ly + 1 == T.th) return ic + T.tw + lx;
     if (lx == 0) return ic + 2 * T.tw + (ly - 1);
     return ic + 2 * T.tw + (T.th - 2) + (ly - 1);
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
 }
 
 __device__ __forceinline__ void ld_relaxed_sys_x2(const unsigned long long *p, unsigned long long &a,
