@@ -423,3 +423,15 @@ def test_inject_mode_c3_and_tiled4_rejected():
     assert_same(g, o)
     with pytest.raises(nb.NocSimError):
         nb.NocSim(W.c1b(inject_mode=1), engine=nb.ENGINE_TILED4)
+
+
+@pytest.mark.parametrize("cfg,cycles", [
+    (W.make(mesh_w=2048, mesh_h=1023, mode=W.MODE_UR, lam=0.02), 30),           # N = 2^21 - 2049: the node-id limit (R32)
+    (W.make(mesh_w=2, mesh_h=2048, mode=W.MODE_LSPD, lam=0.2, sendq_cap=32, l2_sets=4), 600),
+    (W.make(mesh_w=2048, mesh_h=2, mode=W.MODE_LSPD, lam=0.2, sendq_cap=32, l2_sets=4), 600),
+], ids=["max-nodes-ur", "2x2048", "2048x2"])
+def test_maximum_sizes(cfg, cycles):
+    """The largest meshes the ABI accepts (R9, R32: sides up to 2048, N < 2^21):
+    AUTO engine against the oracle."""
+    g, o = both(cfg, cycles)
+    assert_same(g, o)
