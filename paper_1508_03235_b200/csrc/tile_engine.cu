@@ -50,11 +50,6 @@ __device__ __forceinline__ void st_relaxed_x2(unsigned long long *p, unsigned lo
     asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
-// a[p] for a runtime p without indexing a local array (keeps a[] in registers)
-__device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t p)
-{
-    return p == 0u ? a[0] : p == 1u ? a[1] : p == 2u ? a[2] : a[3];
-}
 
 struct TileShape {
     uint32_t x0, y0, tw, th, tn;
@@ -273,7 +268,8 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     const uint32_t np = blockDim.x;
     uint4 *sflit = smem4;
     uint32_t *sfl = reinterpret_cast<uint32_t *>(sflit + 8u * np);
-    unsigned int *scnt = sfl + 2u * np;
+    uint32_t *sna = sfl + 2u * np;   // [4][np]: na[] of each node slot (neighbour slot offsets by port)
+    unsigned int *scnt = sna + 4u * np;
     unsigned int *shist = smem_hist ? scnt + NCOUNTERS : nullptr;
     __shared__ int s_abort;
     __shared__ uint32_t s_busy[2];
@@ -344,6 +340,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             default: m = c.l - 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx - 1, lyy); break;
             }
             if ((intl >> d) & 1u) na[d] = (((d ^ 1u) * np + mi) * 16u) | ((mi * 4u + (d ^ 1u)) << 16);
+            sna[d * np + i] = na[d];
             if ((ext >> d) & 1u) {
                 ExtIn e;
                 e.port = d;
@@ -649,7 +646,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 for (uint32_t k = 0; k < 5; ++k) {
                     const uint32_t p = (ports >> (4u * k)) & 15u;
                     const bool go = ((present >> k) & 1u) && p < 4u && ((intl >> p) & 1u);
-                    const uint32_t w = pick4(na, p & 3u);
+                    const uint32_t w = sna[(p & 3u) * np + i];   // a shared load instead of a select chain
                     sts128_if(go, nf + (w & 0xFFFFu), f[k]);
                     sts8_if(go, no + (w >> 16));
                 }
@@ -766,7 +763,7 @@ __global__ void k_ll_reset(Dev S, uint64_t t)
 // ------------------------------------------------------------------ host side
 size_t tiled_smem_bytes(const Dev &S, uint32_t np, bool with_hist)
 {
-    return (size_t)np * (8u * 16u + 2u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
+    return (size_t)np * (8u * 16u + 6u * 4u) + 4u * NCOUNTERS + (with_hist ? 12u * (size_t)S.nb : 0u);
 }
 
 // Pick TX x TY tiles for one band (<= tiles_budget CTAs, <= TILE_BLOCK_MAX
