@@ -535,7 +535,6 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 #pragma unroll
             for (uint32_t k = 0; k < 5; ++k) {
                 const uint32_t pk = (present >> k) & 1u;
-                bad |= pk & (st - f[k].z > LIFE_MAX ? 1u : 0u);   // R32
                 const uint32_t dst = f_dst(f[k]);
                 const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
                 const uint32_t fc = dst == c.n ? PX : dx != c.x ? (dx > c.x ? PE : PW) : (dy > c.y ? PS : PN);
@@ -545,7 +544,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 ports |= fc << (4u * k);
                 inv |= pk ? k << (4u * fc) : 0u;
             }
-            if (bad) errf |= ERR_AGE;
+            // R32 lifetime limit: a flit's lifetime only grows, so it is checked
+            // where a flit leaves the tile's registers for good -- at ejection,
+            // at a cross-tile hop and at the end of the launch (spill) -- which
+            // flags every overflow by the end of the run, as the oracle does
+            (void)bad;
             uint32_t used = seen & 15u;
             bool has_ej = (seen >> PX) & 1u;
             TRACE_EV(coll ? 16u : 0u);
@@ -631,6 +634,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     unsigned long long *o = ll_out(S, e.sys, e.port, nb1, pstride) + e.outw;
                     if ((used >> e.port) & 1u) {
                         const Flit g = pick5(f, (inv >> (4u * e.port)) & 15u);
+                        if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32, at a cross-tile hop
                         ll_store2(e.sys, o + 2, llw(stn, g.z), llw(stn, g.w));
                         ll_store2(e.sys, o, llw(stn, g.x), llw(stn, g.y));
                     } else {
@@ -657,6 +661,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 const Flit g = pick5(f, (inv >> 16) & 15u);
                 // while draining, quiescence is judged at the end of each
                 // cycle, so the service is not deferred there
+                if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32
                 if (DRAIN) phase3(S, K, c, g, t, acc);
                 else { pend = g; has_pend = true; if (MODE != 0u) prefetch_service(S, c, g); }
             }
@@ -690,7 +695,6 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     const uint64_t tend = t0 + ncyc;
     if (active) {
         if (has_pend) phase3(S, K, c, pend, tend - 1, acc);
-        if (errf) atomicOr(S.err, errf);
         S.fifo_ctl[c.l] = c.qctl;
         if (MODE != 0u) {
             S.core_hot[c.l] = c.hot;
@@ -703,11 +707,14 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
             if (((intl >> d) & 1u) && ((occ >> (8u * d)) & 0xFFu)) {
-                S.flit[be][(size_t)d * S.nloc + c.l] = sflit[(be * 4u + d) * np + i];
+                const uint4 v = sflit[(be * 4u + d) * np + i];
+                if ((uint32_t)tend - v.z > LIFE_MAX) errf |= ERR_AGE;   // R32
+                S.flit[be][(size_t)d * S.nloc + c.l] = v;
                 gfl |= (uint32_t)ste << (8u * d);
             }
         }
         S.flag[be][c.l] = gfl;
+        if (errf) atomicOr(S.err, errf);
         S.flag[be ^ 1u][c.l] = 0u;
     }
     // statistics
