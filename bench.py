@@ -282,6 +282,13 @@ def run_ours(args):
                      "ncu": ncu_info},
         "clocks": ck,
         "sim": {"hash": None, "drops": sum(v for k, v in delta.items() if k.startswith("drops_"))},
+        # the band-edge exchange per cycle of an interior rank (two
+        # edges, W links each way, one 32-byte LL slot per link and cycle written
+        # across NVLink whether or not it carries a flit)
+        "halo": ({"links_per_cycle_per_edge_each_way": cfg["mesh_w"],
+                  "bytes_per_cycle_interior_rank": 2 * 2 * cfg["mesh_w"] * 32,
+                  "engine_exchange": "in-kernel stores into the neighbour rank's slots (CUDA IPC)"}
+                 if world > 1 else None),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # bounded sample: at most ~1e8 node-cycles of oracle work
