@@ -286,8 +286,12 @@ def run_ours(args):
         # edges, W links each way, one 32-byte LL slot per link and cycle written
         # across NVLink whether or not it carries a flit)
         "halo": ({"links_per_cycle_per_edge_each_way": cfg["mesh_w"],
-                  "bytes_per_cycle_interior_rank": 2 * 2 * cfg["mesh_w"] * 32,
-                  "engine_exchange": "in-kernel stores into the neighbour rank's slots (CUDA IPC)"}
+                  "bytes_per_cycle_interior_rank": (2 * 2 * cfg["mesh_w"] * 32 if info1["engine"] in (3, 4)
+                                                    else None),
+                  "engine_exchange": ("TILED: one 32-byte LL slot per band-edge link and cycle, stored into the "
+                                      "neighbour rank's memory (CUDA IPC)" if info1["engine"] in (3, 4) else
+                                      "PERSIST: 16 B flit + 1 flag byte per crossing flit, stored into the "
+                                      "neighbour rank's arrays (CUDA IPC)")}
                  if world > 1 else None),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
