@@ -62,11 +62,15 @@ extern "C" {
                                S:L162)                                         */
 /* engine: which kernel organisation advances the cycles.  Results are
  * bit-identical for every engine. */
-#define NOC_ENGINE_AUTO     0u  /* library picks                                 */
-#define NOC_ENGINE_STEP     1u  /* one fused node-step launch per cycle           */
-#define NOC_ENGINE_PERSIST  2u  /* persistent kernel, neighbour-progress sync     */
+#define NOC_ENGINE_AUTO     0u  /* library picks: TILED if every tile fits (<= 320
+                                   nodes per SM and band), else TILED4, else
+                                   PERSIST                                      */
+#define NOC_ENGINE_STEP     1u  /* one fused node-step launch per cycle (no bands) */
+#define NOC_ENGINE_PERSIST  2u  /* persistent kernel, neighbour-progress sync; any
+                                   mesh size, row bands                         */
 #define NOC_ENGINE_TILED    3u  /* persistent kernel, tiles in shared memory      */
-#define NOC_ENGINE_TILED4   4u  /* as TILED, 4 lanes (one per router port) per node */
+#define NOC_ENGINE_TILED4   4u  /* as TILED, 4 lanes (one per router port) per node;
+                                   not with inject_mode 1                       */
 
 /* A scripted generation event (golden tests; trace replay).
  * At each generation opportunity of node `node` at cycle t (every cycle in UR
@@ -159,8 +163,10 @@ uint32_t noc_sim_abi_version(void);
  * tags homed on them (T mod N in the band).  With world_size = P processes
  * (one GPU each, torchrun), band = rank; the links crossing a band edge are
  * written by the sending GPU directly into the receiving GPU's boundary slots
- * (CUDA IPC over NVLink), NCCL is used for setup and the statistics / hash /
- * drain reductions.  Fills out[128] with a fresh ncclUniqueId (rank 0 calls
+ * (TILED) or link arrays (PERSIST, which also reads the neighbour's progress
+ * counters) through CUDA IPC over NVLink; NCCL is used for setup and the
+ * statistics / hash / drain reductions.  With the centralized directory the
+ * whole location array lives in the directory node's band.  Fills out[128] with a fresh ncclUniqueId (rank 0 calls
  * this and broadcasts it).  Errors: NOC_ENCCL. */
 int noc_sim_nccl_unique_id(uint8_t out[128]);
 
