@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define NOC_SIM_ABI_VERSION 2u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters */
+#define NOC_SIM_ABI_VERSION 3u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base */
 
 /* error codes */
 #define NOC_OK          0
@@ -123,7 +123,12 @@ typedef struct noc_sim_config {
                                   1: NEXT-f4, a flit that will eject frees its
                                   input port for the same cycle.
                                   Not supported by NOC_ENGINE_TILED4          */
-    uint32_t reserved[4];      /* must be 0                                        */
+    uint32_t age_base;         /* test knob: injected flits start at this age
+                                  instead of 0; 0 = the paper's model,
+                                  <= 65535.  Shifts every age equally (ranking
+                                  unchanged) so tests reach ages >= 2048 and the
+                                  R32 age limit (NOC_EOVERFLOW)                  */
+    uint32_t reserved[3];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list

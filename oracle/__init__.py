@@ -60,7 +60,7 @@ class _Config(C.Structure):
         ("script", C.POINTER(_Event)), ("n_script", C.c_uint64), ("route", C.c_uint32),
         ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
-        ("inject_mode", C.c_uint32),
+        ("inject_mode", C.c_uint32), ("age_base", C.c_uint32),
     ]
 
 
@@ -102,6 +102,14 @@ def lib():
         L.orc_l2_line.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
                                   C.POINTER(C.c_uint64)]
         L.orc_loc.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.orc_link.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.orc_fifo.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64),
+                               C.POINTER(C.c_uint64)]
+        L.orc_l1_line.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.orc_script_used.argtypes = [C.c_void_p, C.c_uint32]
+        L.orc_script_used.restype = C.c_int64
+        L.orc_gen.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.orc_poke.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64]
         _lib = L
     return _lib
 
@@ -232,3 +240,40 @@ class Oracle:
         o = (C.c_uint64 * 2)()
         _check(lib().orc_loc(self._h, T, o))
         return tuple(o)
+
+    def link(self, n, d):
+        """Input slot d of node n for the next cycle: None or a dict of the flit."""
+        o = (C.c_uint64 * 8)()
+        _check(lib().orc_link(self._h, n, d, o))
+        if not o[0]:
+            return None
+        return dict(zip(("dst", "src", "kind", "fid", "payload", "age", "inj"), o[1:]))
+
+    def fifo(self, n):
+        """(next-flit index, [packet (kind, dst, payload, nfl) from the head ...])."""
+        ctl = (C.c_uint64 * 2)()
+        pkt = (C.c_uint64 * 4)()
+        _check(lib().orc_fifo(self._h, n, 0xFFFFFFFF, ctl, pkt))
+        out = []
+        for k in range(int(ctl[0])):
+            _check(lib().orc_fifo(self._h, n, k, ctl, pkt))
+            out.append(tuple(int(x) for x in pkt))
+        return int(ctl[1]), out
+
+    def l1_line(self, n, s, w):
+        o = (C.c_uint64 * 4)()
+        _check(lib().orc_l1_line(self._h, n, s, w, o))
+        return tuple(o)
+
+    def script_used(self, n):
+        return int(lib().orc_script_used(self._h, n))
+
+    def gen(self, n, t):
+        """The simulation's generator call for (node, cycle): (fired, dst or tag)."""
+        o = (C.c_uint64 * 2)()
+        _check(lib().orc_gen(self._h, n, t, o))
+        return bool(o[0]), int(o[1])
+
+    def poke(self, field, n=0, i=0, j=0, value=1):
+        """Test-only single-field mutation (fields listed at orc_poke)."""
+        _check(lib().orc_poke(self._h, field, n, i, j, value & 0xFFFFFFFFFFFFFFFF))

@@ -194,6 +194,9 @@ static void enq(orc_sim *s, uint32_t n, uint32_t kind, uint32_t dst, uint32_t pa
     if (dst == n) fail(s, ORC_EASSERT, "packet addressed to its own node");
     if (c->count == s->cfg.sendq_cap) {
         s->c.drops[kind] += 1;
+        /* R21: an LSPD protocol message that is dropped leaves its requester
+         * (or a directory entry) waiting for ever: the run is invalid */
+        if (s->cfg.mode == ORC_MODE_LSPD) fail(s, ORC_EOVERFLOW, "send FIFO overflow in LSPD mode (R21)");
         return;
     }
     Packet *p = &c->fifo[(c->head + c->count) % s->cfg.sendq_cap];
@@ -412,6 +415,30 @@ static void start_access(orc_sim *s, uint32_t n, uint32_t T)
     l2_access(s, n, T);
 }
 
+/* The generator call of node n at cycle t (R25, R35):
+ * fires iff r0 < thr_inj.  UR: the destination is uniform over the N-1 other
+ * nodes, d = mulhi(r1, N-1), skipping self.  LSPD: with probability p_priv
+ * (r1 < thr_priv) a private block T = n*TPN + mulhi(r2, PRIV), else a shared
+ * block T = mulhi(r2, N)*TPN + PRIV + mulhi(r3, TPN-PRIV).  Returns fire. */
+static int gen_draw(const orc_sim *s, uint32_t n, uint64_t t, uint32_t *value)
+{
+    uint32_t r[4];
+    draw(s, n, t, r);
+    if (r[0] >= s->cfg.thr_inj) return 0;
+    if (s->cfg.mode == ORC_MODE_UR) {
+        uint32_t d = mulhi(r[1], s->N - 1);
+        if (d >= n) d += 1;                  /* skip self */
+        *value = d;
+        return 1;
+    }
+    uint32_t TPN = s->cfg.tags_per_node, PRIV = s->cfg.priv_tags;
+    if (r[1] < s->cfg.thr_priv)
+        *value = n * TPN + mulhi(r[2], PRIV);                             /* private */
+    else
+        *value = mulhi(r[2], s->N) * TPN + PRIV + mulhi(r[3], TPN - PRIV); /* shared */
+    return 1;
+}
+
 /* Next script event of node n that is due at cycle t, if any. */
 static int script_next(orc_sim *s, uint32_t n, uint32_t *value)
 {
@@ -431,22 +458,17 @@ static int script_next(orc_sim *s, uint32_t n, uint32_t *value)
 static void phase1(orc_sim *s, uint32_t n)
 {
     Node *c = &s->nodes[n];
-    uint32_t r[4], v;
+    uint32_t v;
 
     if (s->cfg.mode == ORC_MODE_UR) {
         /* uniform-random probes, open loop (R26) */
         if (!s->gen_enabled) return;
-        uint32_t dst;
+        uint32_t dst = 0;
         int fire = 0;
         if (script_next(s, n, &v)) {
             fire = 1; dst = v;
         } else {
-            draw(s, n, s->t, r);
-            if (r[0] < s->cfg.thr_inj) {
-                uint32_t d = mulhi(r[1], s->N - 1);
-                if (d >= n) d += 1;          /* skip self */
-                fire = 1; dst = d;
-            }
+            fire = gen_draw(s, n, s->t, &dst);
         }
         if (fire) {
             s->c.generated += 1;
@@ -467,20 +489,12 @@ static void phase1(orc_sim *s, uint32_t n)
         complete(s, n);
     }
     if (c->mode == M_IDLE && s->gen_enabled) {
-        uint32_t T;
+        uint32_t T = 0;
         int fire = 0;
         if (script_next(s, n, &v)) {
             fire = 1; T = v;
         } else {
-            draw(s, n, s->t, r);
-            if (r[0] < s->cfg.thr_inj) {
-                uint32_t TPN = s->cfg.tags_per_node, PRIV = s->cfg.priv_tags;
-                fire = 1;
-                if (r[1] < s->cfg.thr_priv)
-                    T = n * TPN + mulhi(r[2], PRIV);                          /* private */
-                else
-                    T = mulhi(r[2], s->N) * TPN + PRIV + mulhi(r[3], TPN - PRIV); /* shared */
-            }
+            fire = gen_draw(s, n, s->t, &T);
         }
         if (fire) start_access(s, n, T);
     }
@@ -617,7 +631,8 @@ static void phase2(orc_sim *s, uint32_t n)
         Flit f;
         f.present = 1;
         f.dst = p->dst; f.src = n; f.kind = p->kind; f.fid = c->next;
-        f.age = 0;                               /* "Newly injected flits age is set to zero" */
+        f.age = s->cfg.age_base;                 /* "Newly injected flits age is set to zero";
+                                                    age_base is a test knob, 0 by default */
         f.inj = s->t;
         f.payload = p->payload;
         F[nf++] = f;
@@ -837,6 +852,7 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         set_err("sendq_cap must be a power of two in 1..1024"); return ORC_EINVAL;
     }
     if (cfg->hist_bins == 0 || cfg->hist_bins > 65536) { set_err("hist_bins must be 1..65536"); return ORC_EINVAL; }
+    if (cfg->age_base > AGE_MAX) { set_err("age_base > 65535 (R32)"); return ORC_EINVAL; }
     if (cfg->nfl_ra < 1 || cfg->nfl_ra > 8) { set_err("nfl_ra must be 1..8"); return ORC_EINVAL; }
     uint64_t N = (uint64_t)W * H;
     if (cfg->mode == ORC_MODE_LSPD) {
@@ -1149,4 +1165,99 @@ int orc_loc(const orc_sim *s, uint32_t T, uint64_t out[2])
     if (T >= s->ntags) return ORC_EINVAL;
     out[0] = s->loc[T].holder; out[1] = s->loc[T].pend;
     return ORC_OK;
+}
+
+/* Link input slot d of node n (the inputs of the next cycle to run):
+ * present, dst, src, kind, fid, payload, age, inj. */
+int orc_link(const orc_sim *s, uint32_t n, uint32_t d, uint64_t out[8])
+{
+    if (n >= s->N || d >= 4) return ORC_EINVAL;
+    const Flit *f = &s->nodes[n].in[d];
+    out[0] = (uint64_t)f->present; out[1] = f->dst; out[2] = f->src; out[3] = f->kind;
+    out[4] = f->fid; out[5] = f->payload; out[6] = f->age; out[7] = f->inj;
+    return ORC_OK;
+}
+
+/* Send FIFO of node n: count and next-flit index (out[0..1]); packet k from
+ * the head (k < count): kind, dst, payload, nfl (pkt[0..3]). */
+int orc_fifo(const orc_sim *s, uint32_t n, uint32_t k, uint64_t out[2], uint64_t pkt[4])
+{
+    if (n >= s->N) return ORC_EINVAL;
+    const Node *c = &s->nodes[n];
+    out[0] = c->count; out[1] = c->next;
+    if (k < c->count) {
+        const Packet *p = &c->fifo[(c->head + k) % s->cfg.sendq_cap];
+        pkt[0] = p->kind; pkt[1] = p->dst; pkt[2] = p->payload; pkt[3] = p->nfl;
+    }
+    return ORC_OK;
+}
+
+/* NEXT-f1 L1 line (n, set, way): valid, tag, stamp, owner. */
+int orc_l1_line(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint64_t out[4])
+{
+    if (!s->cfg.l1_sets || n >= s->N || set >= s->cfg.l1_sets || way >= s->cfg.l1_ways) return ORC_EINVAL;
+    const L1Line *L = &s->nodes[n].l1[(uint64_t)set * s->cfg.l1_ways + way];
+    out[0] = (uint64_t)L->valid; out[1] = L->tag; out[2] = L->stamp; out[3] = L->owner;
+    return ORC_OK;
+}
+
+/* Script events consumed by node n. */
+int64_t orc_script_used(const orc_sim *s, uint32_t n)
+{
+    return n < s->N ? (int64_t)s->nodes[n].script_used : -1;
+}
+
+/* The generator call the simulation makes for node n at cycle t (gen_draw):
+ * out[0] = fired, out[1] = UR destination or LSPD block tag. */
+int orc_gen(const orc_sim *s, uint32_t n, uint64_t t, uint64_t out[2])
+{
+    if (n >= s->N) return ORC_EINVAL;
+    uint32_t v = 0;
+    out[0] = (uint64_t)gen_draw(s, n, t, &v);
+    out[1] = v;
+    return ORC_OK;
+}
+
+/* Test-only mutation of one state field (hash sensitivity pins):
+ *   field 0 link slot (n, i=d) age += value      1 link slot (n, i=d) payload ^= value
+ *   2 core (n) start += value                    3 core (n) mode = value
+ *   4 L2 line (n, i=set, j=way) stamp += value   5 loc entry (T=n) pend += value
+ *   6 FIFO packet (n, i=k) payload ^= value      7 FIFO next (n) = value
+ *   8 counter index i += value                   9 histogram (i=which, j=bin) += value
+ *  10 cycle += value                            11 L1 line (n, i, j) owner ^= value
+ *  12 core (n) rx += value                      13 core (n) ready += value */
+int orc_poke(orc_sim *s, uint32_t field, uint32_t n, uint32_t i, uint32_t j, uint64_t value)
+{
+    Node *c = n < s->N ? &s->nodes[n] : NULL;
+    switch (field) {
+    case 0: if (!c || i >= 4) return ORC_EINVAL; c->in[i].age += value; return ORC_OK;
+    case 1: if (!c || i >= 4) return ORC_EINVAL; c->in[i].payload ^= (uint32_t)value; return ORC_OK;
+    case 2: if (!c) return ORC_EINVAL; c->start += value; return ORC_OK;
+    case 3: if (!c) return ORC_EINVAL; c->mode = (int)value; return ORC_OK;
+    case 4:
+        if (!c || s->cfg.mode != ORC_MODE_LSPD || i >= s->cfg.l2_sets || j >= s->cfg.l2_ways) return ORC_EINVAL;
+        c->l2[(uint64_t)i * s->cfg.l2_ways + j].stamp += value; return ORC_OK;
+    case 5: if (n >= s->ntags) return ORC_EINVAL; s->loc[n].pend += (uint32_t)value; return ORC_OK;
+    case 6:
+        if (!c || i >= c->count) return ORC_EINVAL;
+        c->fifo[(c->head + i) % s->cfg.sendq_cap].payload ^= (uint32_t)value; return ORC_OK;
+    case 7: if (!c) return ORC_EINVAL; c->next = (uint32_t)value; return ORC_OK;
+    case 8: {
+        int ncnt = (int)((sizeof(orc_counters) - sizeof(int64_t)) / sizeof(int64_t));
+        if ((int)i >= ncnt) return ORC_EINVAL;
+        (&s->c.generated)[i] += (int64_t)value; return ORC_OK;
+    }
+    case 9: {
+        uint64_t *hs[3] = { s->hl, s->hd, s->ha };
+        if (i >= 3 || j >= s->cfg.hist_bins) return ORC_EINVAL;
+        hs[i][j] += value; return ORC_OK;
+    }
+    case 10: s->t += value; s->c.cycle = (int64_t)s->t; return ORC_OK;
+    case 11:
+        if (!c || !s->cfg.l1_sets || i >= s->cfg.l1_sets || j >= s->cfg.l1_ways) return ORC_EINVAL;
+        c->l1[(uint64_t)i * s->cfg.l1_ways + j].owner ^= (uint32_t)value; return ORC_OK;
+    case 12: if (!c) return ORC_EINVAL; c->rx += (uint32_t)value; return ORC_OK;
+    case 13: if (!c) return ORC_EINVAL; c->ready += value; return ORC_OK;
+    }
+    return ORC_EINVAL;
 }

@@ -69,6 +69,7 @@ typedef struct {
     uint32_t l1_sets, l1_ways;   /* NEXT-f1 private L1 (Table III); 0 sets = none */
     uint32_t l1_miss_lat;        /* "L1 miss cycle" countdown, >= 1 */
     uint32_t inject_mode;        /* 0: R7; 1: an ejecting flit frees its slot (NEXT-f4) */
+    uint32_t age_base;           /* test knob: age of a newly injected flit (0 = P:L259) */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */
@@ -123,6 +124,19 @@ int  orc_l2_line(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way,
                  uint64_t out[3]);
 /* Directory entry of tag T: holder (UINT32_MAX = none) and pend. */
 int  orc_loc(const orc_sim *s, uint32_t T, uint64_t out[2]);
+
+/* Link input slot d of node n: present, dst, src, kind, fid, payload, age, inj. */
+int  orc_link(const orc_sim *s, uint32_t n, uint32_t d, uint64_t out[8]);
+/* Send FIFO of n: out = {count, next}; pkt = packet k from the head {kind, dst, payload, nfl}. */
+int  orc_fifo(const orc_sim *s, uint32_t n, uint32_t k, uint64_t out[2], uint64_t pkt[4]);
+/* NEXT-f1 L1 line: valid, tag, stamp, owner. */
+int  orc_l1_line(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint64_t out[4]);
+/* Script events consumed by node n (-1 if n is out of range). */
+int64_t orc_script_used(const orc_sim *s, uint32_t n);
+/* The simulation's generator call for (n, t): out = {fired, UR dst or LSPD tag}. */
+int  orc_gen(const orc_sim *s, uint32_t n, uint64_t t, uint64_t out[2]);
+/* Test-only single-field mutation (hash sensitivity pins); fields in noc_oracle.c. */
+int  orc_poke(orc_sim *s, uint32_t field, uint32_t n, uint32_t i, uint32_t j, uint64_t value);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ enum : uint32_t {
     C_DROPS = 23, C_L1HIT = 31, C_L1MISS, C_WBSENT, C_WBRCVD, NCOUNTERS = 35
 };
 // error flags
-enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8 };
+enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8, ERR_DROP = 16 };
 
 constexpr uint32_t AGE_MAX = 65535u;   // R32
 constexpr uint32_t LIFE_MAX = (1u << 27) - 1u;   // R32: flit lifetime t - inj
@@ -149,6 +149,7 @@ struct Dev {
     uint32_t dir_mode, dir_node;      // NEXT-f3: central directory at dir_node (R40)
     uint32_t l1_sets, l1_ways, l1_miss_lat;   // NEXT-f1 private L1 (R42); 0 sets = none
     uint32_t inject_mode;             // NEXT-f4: an ejecting flit frees its slot (R43)
+    uint32_t age_base;                // test knob: age of an injected flit (0 = P:L259)
     uint64_t loc_n;                   // directory entries held by this band
     uint32_t qcap, nb, seed_lo, seed_hi;
     uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi

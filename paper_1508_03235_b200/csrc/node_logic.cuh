@@ -73,7 +73,13 @@ __device__ __forceinline__ void enq(const Dev &S, const Sink &K, NodeCtx &c, uin
                                     uint32_t payload, uint32_t nfl)
 {
     uint32_t h = q_head(c.qctl), cnt = q_count(c.qctl);
-    if (cnt == S.qcap) { K.cnt(S, C_DROPS + kind); return; }
+    if (cnt == S.qcap) {
+        K.cnt(S, C_DROPS + kind);
+        // R21: in LSPD mode a dropped protocol message would leave a core or a
+        // directory entry waiting for ever, so the run is invalid: poison it
+        if (S.mode != 0u) atomicOr(S.err, ERR_DROP);
+        return;
+    }
     uint32_t slot = (h + cnt) & (S.qcap - 1u);
     const uint2 pkt = make_uint2(dst | (kind << 21) | (nfl << 24), payload);
     S.fifo_pkt[(size_t)c.l * S.qcap + slot] = pkt;
@@ -693,6 +699,7 @@ __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t n
     const uint2 p = c.head;
     const uint32_t nfl = (p.x >> 24) & 15u;
     out = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
+    f_set_age(out, S.age_base);
     ++acc.injected;
     ++nx;
     if (nx == nfl) {

@@ -133,6 +133,7 @@ static int validate(const noc_sim_config *c)
     for (int i = 0; i < 4; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->inject_mode > 1) return fail(NOC_EINVAL, "inject_mode out of range");
+    if (c->age_base > AGE_MAX) return fail(NOC_EINVAL, "age_base > 65535 (R32)");
     if (c->inject_mode && c->engine == NOC_ENGINE_TILED4)
         return fail(NOC_EINVAL, "inject_mode 1 needs five flit lanes per router: not with the TILED4 engine");
     if (c->mode == NOC_MODE_LSPD && c->l1_sets &&
@@ -195,6 +196,7 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.l1_ways = cfg->l1_ways;
     D.l1_miss_lat = cfg->l1_miss_lat;
     D.inject_mode = cfg->inject_mode;
+    D.age_base = cfg->age_base;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
@@ -508,6 +510,7 @@ static int check_err(noc_sim *s)
             snprintf(b, sizeof b, "boundary / neighbour wait timed out (flags 0x%08x)", err);
             return fail(NOC_ECUDA, b);
         }
+        if (err & ERR_DROP) return fail(NOC_EOVERFLOW, "send FIFO overflow in LSPD mode (R21: a dropped protocol message)");
         if (err & (ERR_AGE | ERR_PEND)) return fail(NOC_EOVERFLOW, "field width exceeded (flit age, lifetime or pend)");
         return fail(NOC_ECUDA, "model assertion failed on device (protocol / EV holder)");
     }

@@ -94,11 +94,11 @@ def test_c4_saturated_208():
     W.make(mesh_w=2, mesh_h=37, mode=W.MODE_UR, lam=0.3, prio=W.PRIO_OLDEST),
     W.make(mesh_w=53, mesh_h=3, mode=W.MODE_LSPD, lam=0.2, l2_sets=3, l2_ways=3, sendq_cap=32),
     W.make(mesh_w=5, mesh_h=7, mode=W.MODE_LSPD, lam=0.5, l2_hit_lat=0, nfl_ra=1, sendq_cap=32),
-    W.make(mesh_w=6, mesh_h=6, mode=W.MODE_LSPD, lam=0.3, nfl_ra=8, sendq_cap=2, hist_bins=1),
+    W.make(mesh_w=6, mesh_h=6, mode=W.MODE_LSPD, lam=0.3, nfl_ra=8, sendq_cap=4, hist_bins=1),
     W.make(mesh_w=9, mesh_h=4, mode=W.MODE_LSPD, lam=1.0, l2_sets=1, l2_ways=16, sendq_cap=64,
            tags_per_node=4, priv_tags=1, mem_lat=1),
     W.make(mesh_w=300, mesh_h=7, mode=W.MODE_LSPD, lam=0.1, hist_bins=64, seed=2 ** 40 + 7),
-], ids=["2x2", "2x37-oldest", "53x3", "hitlat0-nfl1", "nfl8-q2-nb1", "1set16way", "300x7-bigseed"])
+], ids=["2x2", "2x37-oldest", "53x3", "hitlat0-nfl1", "nfl8-q4-nb1", "1set16way", "300x7-bigseed"])
 @pytest.mark.parametrize("engine", ENGINES)
 def test_edge_configurations(cfg, engine):
     g, o = both(cfg, 2500, engine)
@@ -328,7 +328,7 @@ def test_c4_sweep_endpoints(mode, lam):
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("cfg", [
     W.c1b(dir_mode=W.DIR_CENTRAL, dir_node=5, lam=0.05),
-    W.lspd(24, 20, lam=0.02, dir_mode=W.DIR_CENTRAL, dir_node=10 * 24 + 12, sendq_cap=64),
+    W.lspd(24, 20, lam=0.02, dir_mode=W.DIR_CENTRAL, dir_node=10 * 24 + 12, sendq_cap=512),
 ], ids=["c1b", "lspd24x20"])
 def test_centralized_directory(cfg, engine):
     """NEXT-f3: the paper's centralized location array (R40)
@@ -337,22 +337,20 @@ def test_centralized_directory(cfg, engine):
     assert_same(g, o)
     st = g.stats()[0]
     assert st["dir_searches"] > 0 and st["evs_received"] > 0
-    if cfg["mesh_w"] == 4:
-        # 16 cores stay below the directory node's one ejection per cycle; at
-        # 24x20 the closed loop offers ~4 directory accesses per cycle and the
-        # directory node's send FIFO overflows (the hot spot of P:L71, R21
-        # drop counters), identically on both sides
-        assert sum(v for k, v in st.items() if k.startswith("drops_")) == 0
+    # the directory node's FIFO holds up to one reply per requester (R19), so
+    # sendq_cap >= N + 2 never overflows; a smaller one would poison the run
+    # on both sides (R21, test_lspd_fifo_overflow_is_an_error_on_both_sides)
+    assert sum(v for k, v in st.items() if k.startswith("drops_")) == 0
 
 
 def test_centralized_directory_c3_and_bands():
     """C3 with the directory at the centre node (the hot spot the paper warns
     about), and the same across 4 virtual bands (the directory band
     receives every DA over band edges)."""
-    cfg = W.c3(lam=0.002, dir_mode=W.DIR_CENTRAL, dir_node=104 * 208 + 104, sendq_cap=256)
+    cfg = W.c3(lam=0.002, dir_mode=W.DIR_CENTRAL, dir_node=104 * 208 + 104, sendq_cap=1024)
     g, o = both(cfg, 600)
     assert_same(g, o)
-    cfg = W.lspd(22, 19, lam=0.02, dir_mode=W.DIR_CENTRAL, dir_node=9 * 22 + 11, sendq_cap=64)
+    cfg = W.lspd(22, 19, lam=0.02, dir_mode=W.DIR_CENTRAL, dir_node=9 * 22 + 11, sendq_cap=512)
     for engine in (nb.ENGINE_TILED, nb.ENGINE_PERSIST):
         g = nb.NocSim(cfg, bands=4, engine=engine)
         o = Oracle(cfg)
