@@ -128,6 +128,17 @@ def oracle_rate(cfg, cycles):
     return n * cycles / dt, dt
 
 
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -139,7 +150,8 @@ def run_reference(args):
     desc, fn = WORKLOADS[args.workload]
     cfg = fn(seed=1)
     n = cfg["mesh_w"] * cfg["mesh_h"]
-    cyc = args.ref_cycles_per_step
+    # a bounded sample per step: about 2e7 node-cycles (C3: 200 cycles, C5: 19)
+    cyc = args.ref_cycles_per_step or max(2, min(200, int(2e7 // n)))
     from oracle import Oracle
     o = Oracle(cfg)
     for _ in range(args.warmup):
@@ -224,13 +236,14 @@ def run_ours(args):
 
     # roofline of the dominant (only) kernel in the timed region
     peak, peak_src = peaks()
-    B, rates = b_alg(delta, nodecycles, cfg["l2_ways"] if cfg["mode"] == W.MODE_LSPD else 2)
+    # stats() sums the counters over all ranks: rates are per node-cycle of the whole job
+    B, rates = b_alg(delta, nodecycles * world, cfg["l2_ways"] if cfg["mode"] == W.MODE_LSPD else 2)
     launches = info1["kernel_launches"] - info0["kernel_launches"]
     # the TILED engines also launch the LL-slot refresh kernel before each
     # node-step launch (one per band of this process)
     gpu_launches = launches * (2 if info1["engine"] in (3, 4) else 1)
     per_launch_ms = dev_ms / max(launches, 1)
-    achieved = B * nodecycles / (dev_ms / 1e3) / 1e9
+    achieved = B * nodecycles / (dev_ms / 1e3) / 1e9          # per GPU (this rank's nodes)
     traffic, ncu_info = None, None
     tf = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.workload)
     if os.path.exists(tf):
@@ -294,13 +307,29 @@ def run_ours(args):
                                       "neighbour rank's arrays (CUDA IPC)")}
                  if world > 1 else None),
     }
+    # the median over 5 fresh creations (same warm-up, one step each)
+    fresh = None
+    if world == 1 and args.fresh > 0:
+        per = []
+        for _ in range(args.fresh):
+            f = pkg.NocSim(cfg, device=dev, engine=eng)
+            f.run(cyc * args.warmup)
+            flush_l2(l2buf)
+            torch.cuda.synchronize()
+            per.append(f.run_timed(cyc))
+            f.close()
+        fresh = {"creations": len(per), "median_ms_per_step": statistics.median(per),
+                 "median_value": n * cyc / (statistics.median(per) / 1e3),
+                 "min_ms_per_step": min(per), "max_ms_per_step": max(per)}
+    line["fresh_creations"] = fresh
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # bounded sample: at most ~1e8 node-cycles of oracle work
         ccyc = max(20, min(args.cpu_cycles, int(1e8 // (cfg["mesh_w"] * cfg["mesh_h"]))))
         v, dt = oracle_rate(cfg, ccyc)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s cycles 0-%d from a fresh state, 1 host thread (%.1f s)" % (
-                                    args.workload, ccyc, dt)}
+                                    args.workload, ccyc, dt),
+                                "host_cpu": host_cpu(), "host_nproc": os.cpu_count()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     sim.close()
@@ -315,21 +344,46 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c3 on one GPU, c5 (strong scaling) on several")
     ap.add_argument("--cycles-per-step", type=int, default=2000)
-    ap.add_argument("--ref-cycles-per-step", type=int, default=200)
+    ap.add_argument("--ref-cycles-per-step", type=int, default=0, help="0: ~2e7 node-cycles per step")
     ap.add_argument("--cpu-cycles", type=int, default=2000)
     ap.add_argument("--engine", default="auto", choices=sorted(ENGINES))
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fresh", type=int, default=5, help="fresh creations for the median (SURVEY 8(d.4)); 0 = off")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="N>1: weak (mesh height x N, default) or strong (fixed mesh; default for c5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload is None:
+        # one GPU: the 208x208 single-B200 configuration (BASELINE configs[2]);
+        # several: the 1024x1024 mesh in row bands (configs[4], strong scaling)
+        args.workload = "c3" if args.gpus == 1 else "c5"
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_ours(args)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on this node and relay rank 0's line."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write("bench.py: --gpus %d needs %d CUDA devices, this box has %d\n" % (args.gpus, args.gpus, have))
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

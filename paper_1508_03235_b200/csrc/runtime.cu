@@ -130,7 +130,7 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    for (int i = 0; i < 4; ++i)
+    for (size_t i = 0; i < sizeof c->reserved / sizeof c->reserved[0]; ++i)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->inject_mode > 1) return fail(NOC_EINVAL, "inject_mode out of range");
     if (c->age_base > AGE_MAX) return fail(NOC_EINVAL, "age_base > 65535 (R32)");
@@ -535,6 +535,15 @@ static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
             for (int b = 0; b < s->nb; ++b) CU(launch_ll_refresh(s->D[b], s->t + done, s->stream));
+            // ranks: every rank's refresh completes before any rank's kernel
+            // starts, else a fast neighbour's first boundary stores (stamp t0+1)
+            // could be re-stamped t0-1 by this rank's late refresh (a stream-
+            // ordered barrier: the all-reduce completes only once every rank
+            // enqueued it after its own refresh)
+            if (s->world > 1) {
+                int rc0 = allreduce_u32(s, s->d_scratch + DRAIN_CHUNK + 1, 1);
+                if (rc0) return rc0;
+            }
             uint32_t *act = activity ? activity + done : nullptr;
             e = s->engine == NOC_ENGINE_TILED4
                     ? launch_tiled4(s->set, s->t + done, k, s->t_tpad, s->t_smem_hist, act, s->stream)
@@ -604,6 +613,11 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
     uint64_t t0 = s->t, k = 0;
     int q = 0, rc;
     set_gen(s, 0);
+    // generation is re-enabled on every exit path (a scope guard)
+    struct GenGuard {
+        noc_sim *s;
+        ~GenGuard() { set_gen(s, 1); }
+    } guard{s};
     // quiescent already?
     CU(cudaMemsetAsync(s->d_scratch, 0, 4, s->stream));
     for (int b = 0; b < s->nb; ++b) CU(launch_busy_count(s->D[b], s->t, s->d_scratch, s->stream));
@@ -617,7 +631,7 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
         uint32_t chunk = (uint32_t)std::min<uint64_t>(DRAIN_CHUNK, max_cycles - k);
         CU(cudaMemsetAsync(s->d_scratch, 0, sizeof(uint32_t) * chunk, s->stream));
         rc = advance(s, chunk, s->d_scratch);
-        if (rc) { set_gen(s, 1); return rc; }
+        if (rc) return rc;
         if ((rc = allreduce_u32(s, s->d_scratch, chunk))) return rc;
         CU(cudaMemcpyAsync(act.data(), s->d_scratch, sizeof(uint32_t) * chunk, cudaMemcpyDeviceToHost, s->stream));
         CU(cudaStreamSynchronize(s->stream));
@@ -638,7 +652,6 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
             k += chunk;
         }
     }
-    set_gen(s, 1);
     if (used) *used = k;
     if (drained) *drained = q;
     return check_err(s);

@@ -171,21 +171,26 @@ __device__ __forceinline__ unsigned long long *ll_out(const Dev &S, bool band_ed
 // 32 injection, 64 flits present, 128 boundary node).
 #ifdef NOC_TRACE
 constexpr uint32_t TRACE_CYC = 1024, TRACE_WARPS = 1536;
-__device__ uint4 g_trace[TRACE_CYC][TRACE_WARPS];
+__device__ uint4 g_trace[TRACE_CYC][TRACE_WARPS][2];
 __device__ int g_trace_on;
-#define TRACE_DECL long long tr_c0 = clock64(), tr_x = 0; uint32_t tr_ev = 0, tr_h = 0, tr_q = 0;
+#define TRACE_DECL long long tr_c0 = clock64(), tr_x = 0, tr_p3 = 0, tr_p1 = 0, tr_pub = 0; uint32_t tr_ev = 0, tr_h = 0, tr_q = 0;
 #define TRACE_EV(b) tr_ev |= (b);
-#define TRACE_P1_BEGIN tr_h = c.hot; tr_q = c.qctl;
-#define TRACE_P1_END tr_ev |= (c.hot != tr_h ? 2u : 0u) | (c.qctl != tr_q ? 4u : 0u);
+#define TRACE_P1_BEGIN tr_p3 = clock64(); tr_h = c.hot; tr_q = c.qctl;
+#define TRACE_P1_END tr_p1 = clock64(); tr_ev |= (c.hot != tr_h ? 2u : 0u) | (c.qctl != tr_q ? 4u : 0u);
 #define TRACE_EXT_DONE tr_x = clock64();
+#define TRACE_PUB_DONE tr_pub = clock64();
+#define TRACE_OFS(v) __reduce_max_sync(0xFFFFFFFFu, (v) ? (uint32_t)((v) - tr_c0) : 0u)
 #define TRACE_END                                                                                       \
     {                                                                                                   \
         const uint32_t ev = __reduce_or_sync(0xFFFFFFFFu, tr_ev);                                       \
         const long long tr_a = clock64();                                                               \
-        const uint32_t xw = __reduce_max_sync(0xFFFFFFFFu, tr_x ? (uint32_t)(tr_x - tr_c0) : 0u);       \
+        const uint32_t xw = TRACE_OFS(tr_x), p3w = TRACE_OFS(tr_p3), p1w = TRACE_OFS(tr_p1),            \
+                       pbw = TRACE_OFS(tr_pub);                                                         \
         const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);                        \
-        if (g_trace_on && (threadIdx.x & 31u) == 0u && cc < TRACE_CYC && wg < TRACE_WARPS)              \
-            g_trace[cc][wg] = make_uint4((uint32_t)tr_c0, (uint32_t)(tr_a - tr_c0), ev, xw);            \
+        if (g_trace_on && (threadIdx.x & 31u) == 0u && cc < TRACE_CYC && wg < TRACE_WARPS) {            \
+            g_trace[cc][wg][0] = make_uint4((uint32_t)tr_c0, (uint32_t)(tr_a - tr_c0), ev, xw);         \
+            g_trace[cc][wg][1] = make_uint4(p3w, p1w, pbw, 0u);                                         \
+        }                                                                                               \
     }
 extern "C" int noc_trace_ctl(int on, void *host, size_t bytes)
 {
@@ -198,6 +203,7 @@ extern "C" int noc_trace_ctl(int on, void *host, size_t bytes)
 #define TRACE_P1_BEGIN
 #define TRACE_P1_END
 #define TRACE_EXT_DONE
+#define TRACE_PUB_DONE
 #define TRACE_END
 #endif
 
@@ -642,6 +648,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     }
                 }
             }
+            TRACE_PUB_DONE
             // (5) flits that stay in the tile: predicated shared-memory stores
             // into the neighbour's slot opp(p) of cycle t+1
             if (used & intl) {

@@ -44,3 +44,15 @@ def test_bench_json_line_on_gpu(engine):
                   "--engine", engine)
     assert KEYS <= set(d) and {"roofline", "cpu_baseline", "clocks", "gpu_launches"} <= set(d)
     assert d["value"] > 0 and d["gpu_launches"] > 0 and 0 < d["roofline"]["frac"] < 1.5
+
+
+def test_gpus_beyond_the_box_is_an_error():
+    """`bench.py --gpus N` outside torchrun spawns N ranks; with fewer than N
+    devices it fails with a clear message instead of reporting one GPU."""
+    import torch
+    n = max(2, torch.cuda.device_count() + 1)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK")})
+    assert out.returncode == 2 and "needs %d CUDA devices" % n in out.stderr
+    assert not [ln for ln in out.stdout.splitlines() if ln.startswith("{")]

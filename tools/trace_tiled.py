@@ -26,13 +26,14 @@ info = s.info()
 lib.noc_trace_ctl(1, None, 0)
 ms = s.run_timed(TRACE_CYC)
 lib.noc_trace_ctl(0, None, 0)
-buf = np.zeros((TRACE_CYC, TRACE_WARPS, 4), dtype=np.uint32)
+buf = np.zeros((TRACE_CYC, TRACE_WARPS, 8), dtype=np.uint32)
 assert lib.noc_trace_ctl(0, buf.ctypes.data, buf.nbytes) == 0
 grid, block = info["grid"], info["block"]
 wpc = block // 32
 nw = grid * wpc
 tr = buf[:, :nw, :].astype(np.int64)
 start, arrive, ev, extw = tr[..., 0], tr[..., 1], tr[..., 2], tr[..., 3]
+p3w, p1w, pubw = tr[..., 4], tr[..., 5], tr[..., 6]
 print("%s: %.3f us/cycle (traced run), grid %d x %d warps" % (wl, ms * 1e3 / TRACE_CYC, grid, wpc))
 # per CTA: cycle length from warp 0's start clocks (same SM clock)
 st0 = start[:, ::wpc]
@@ -62,5 +63,12 @@ bx = extw.reshape(TRACE_CYC, grid, wpc)
 bnd = ((e3 >> 7) & 1) == 1
 print("boundary warps: ext-complete offset median %d p90 %d; arrival median %d" % (
     np.median(bx[bnd]), np.percentile(bx[bnd], 90), np.median(arr[bnd])))
-print("interior warps arrival median %d" % np.median(arr[~bnd]))
+print("interior warps arrival median %d" % (np.median(arr[~bnd]) if (~bnd).any() else -1))
+for nm, msk in (("boundary", bnd), ("interior", ~bnd)):
+    if not msk.any():
+        continue
+    q = lambda a: "%5d %5d %5d" % (np.percentile(a[msk], 50), np.percentile(a[msk], 90), a[msk].mean())
+    print("%s warps (p50 p90 mean clk from cycle start): phase3 done %s | phase1 done %s | ext done %s | "
+          "published %s | barrier %s" % (nm, q(p3w.reshape(arr.shape)), q(p1w.reshape(arr.shape)),
+                                          q(bx), q(pubw.reshape(arr.shape)), q(arr)))
 print("last warp is a boundary warp in %.1f%% of CTA-cycles" % (100 * ((lastev >> 7) & 1).mean()))
