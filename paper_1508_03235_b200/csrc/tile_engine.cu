@@ -173,10 +173,10 @@ __device__ __forceinline__ unsigned long long *ll_out(const Dev &S, bool band_ed
 constexpr uint32_t TRACE_CYC = 1024, TRACE_WARPS = 1536;
 __device__ uint4 g_trace[TRACE_CYC][TRACE_WARPS][2];
 __device__ int g_trace_on;
-#define TRACE_DECL long long tr_c0 = clock64(), tr_x = 0, tr_p3 = 0, tr_p1 = 0, tr_pub = 0; uint32_t tr_ev = 0, tr_h = 0, tr_q = 0;
+#define TRACE_DECL long long tr_c0 = clock64(), tr_x = 0, tr_p3 = 0, tr_p1 = 0, tr_pub = 0; uint32_t tr_ev = 0;
 #define TRACE_EV(b) tr_ev |= (b);
-#define TRACE_P1_BEGIN tr_p3 = clock64(); tr_h = c.hot; tr_q = c.qctl;
-#define TRACE_P1_END tr_p1 = clock64(); tr_ev |= (c.hot != tr_h ? 2u : 0u) | (c.qctl != tr_q ? 4u : 0u);
+#define TRACE_P3_DONE tr_p3 = clock64();
+#define TRACE_P1_DONE tr_p1 = clock64();
 #define TRACE_EXT_DONE tr_x = clock64();
 #define TRACE_PUB_DONE tr_pub = clock64();
 #define TRACE_OFS(v) __reduce_max_sync(0xFFFFFFFFu, (v) ? (uint32_t)((v) - tr_c0) : 0u)
@@ -200,8 +200,8 @@ extern "C" int noc_trace_ctl(int on, void *host, size_t bytes)
 #else
 #define TRACE_DECL
 #define TRACE_EV(b)
-#define TRACE_P1_BEGIN
-#define TRACE_P1_END
+#define TRACE_P3_DONE
+#define TRACE_P1_DONE
 #define TRACE_EXT_DONE
 #define TRACE_PUB_DONE
 #define TRACE_END
@@ -236,6 +236,29 @@ __device__ __forceinline__ void sts8_if(bool c, uint32_t a)
                  ::"r"((uint32_t)c), "r"(a), "r"(1u) : "memory");
 }
 
+// First choice of a flit with destination dst at node (n, x, y): eject at the
+// destination, else the x-port while dx != 0, else the y-port (PMDR).
+// Written as predicated selects (the nested ternary compiled to a branch
+// region per slot).
+__device__ __forceinline__ uint32_t first_port(uint32_t dst, uint32_t n, uint32_t x, uint32_t y, uint32_t W,
+                                               uint32_t wmagic)
+{
+    const uint32_t dy = __umulhi(dst, wmagic), dx = dst - dy * W;
+    uint32_t p;
+    asm("{\n\t.reg .pred q;\n\t.reg .u32 px;\n\t"
+        "setp.gt.u32 q, %2, %4;\n\t"
+        "selp.u32 %0, 1, 0, q;\n\t"          // y-port: S (1) if dy > y else N (0)
+        "setp.gt.u32 q, %1, %3;\n\t"
+        "selp.u32 px, 2, 3, q;\n\t"          // x-port: E (2) if dx > x else W (3)
+        "setp.ne.u32 q, %1, %3;\n\t"
+        "selp.u32 %0, px, %0, q;\n\t"
+        "setp.eq.u32 q, %5, %6;\n\t"
+        "selp.u32 %0, 4, %0, q;\n\t"          // eject (4) at the destination
+        "}"
+        : "=r"(p) : "r"(dx), "r"(dy), "r"(x), "r"(y), "r"(dst), "r"(n));
+    return p;
+}
+
 // f[k] for a runtime k in [0, 5) without indexing a local array
 __device__ __forceinline__ Flit pick5(const Flit (&f)[5], uint32_t k)
 {
@@ -266,10 +289,15 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 {
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     // this CTA's band and tile
+    // FEAT bit 2: several bands in this launch (virtual bands).  With one band
+    // the parameters are read at constant offsets (constant-bank operands of
+    // the instructions themselves) instead of indexed constant loads that the
+    // register-starved loop would otherwise re-issue every cycle
     uint32_t band = 0;
-    while (band + 1 < P.nbands && blockIdx.x >= P.tile0[band + 1]) ++band;
-    const Dev &S = P.d[band];
-    const uint32_t tile = blockIdx.x - P.tile0[band];
+    if (FEAT & 4u)
+        while (band + 1 < P.nbands && blockIdx.x >= P.tile0[band + 1]) ++band;
+    const Dev &S = P.d[(FEAT & 4u) ? band : 0u];
+    const uint32_t tile = blockIdx.x - ((FEAT & 4u) ? P.tile0[band] : 0u);
     extern __shared__ uint4 smem4[];
     const uint32_t np = blockDim.x;
     uint4 *sflit = smem4;
@@ -412,49 +440,55 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         }
     };
     const bool windows = MODE != 0u && S.gen && !S.has_script;
-    if (windows) {
+    // windows for cycle tn: idle cores and cores whose wait expires at tn
+    auto need_window = [&](uint64_t tn) {
+        if (!active) return false;
         const uint32_t mode = core_mode(c.hot);
-        const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t0) & 0x1FFFFFFFu) == 0u);
-        refresh(active && (mode == MIDLE || expiring), t0);
-    }
-    __syncthreads();
-
+        const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)tn) & 0x1FFFFFFFu) == 0u);
+        if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
+        return (mode == MIDLE || expiring) && (uint32_t)tn - wbase >= 32u;
+    };
     const uint32_t pstride = 16u * S.nloc;
     Sink K{scnt, shist, true};
     Acc acc = {0, 0, 0, 0};
-    Flit pend = {0, 0, 0, 0};
-    bool has_pend = false;
     const uint32_t own_f = fa + i * 16u, own_o = oa + i * 4u;
     const ExtIn &e0 = ex[0], &e1 = ex[1];
+
+    // Cycle order (DESIGN 6.3): Phase 1 of cycle t runs at the END of cycle
+    // t-1 (after its Phase 2 and 3; it reads only node-local state and the
+    // draw of (n, t)), so a cycle starts directly with the latch and the
+    // routing, and the boundary outputs -- the critical path of the
+    // neighbouring tiles -- are published first.  The boundary polls of cycle
+    // t+1 are issued right after cycle t's outputs are published, so their
+    // latency overlaps the rest of cycle t (Phase 3, Phase 1 of t+1, the
+    // barrier).  Phase 1 of the first cycle runs in the prologue.
+    unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0w = 0, b1w = 0, b2w = 0, b3w = 0;
+    if (active && ext) {
+        const unsigned long long *const llp = S.ll + (size_t)b0 * pstride;
+        ll_load2(e0.sys, llp + e0.inw, a0, a1);
+        ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
+        if (e1.port != NOPORT) {
+            ll_load2(e1.sys, llp + e1.inw, b0w, b1w);
+            ll_load2(e1.sys, llp + e1.inw + 2, b2w, b3w);
+        }
+    }
+    if (windows) refresh(need_window(t0), t0);
+    if (active) {
+        if (MODE == 0u) phase1_ur(S, K, c, t0);
+        else phase1_lspd_win<MODE == 2u>(S, K, c, t0, wbase, wmask);
+    }
+    __syncthreads();
 
     for (uint32_t cc = 0; cc < ncyc; ++cc) {
         const uint64_t t = t0 + cc;
         const uint32_t pb = (uint32_t)t & 1u, nb1 = pb ^ 1u;
         const uint32_t st = (uint32_t)t, stn = st + 1u;
+        const bool last = cc + 1u == ncyc;
         bool busy = false;
         TRACE_DECL
         if (active) {
             const unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
-            // (0) issue the boundary polls first (all four words of each slot)
-            unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0w = 0, b1w = 0, b2w = 0, b3w = 0;
-            if (ext) {
-                ll_load2(e0.sys, llp + e0.inw, a0, a1);
-                ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
-                if (e1.port != NOPORT) {
-                    ll_load2(e1.sys, llp + e1.inw, b0w, b1w);
-                    ll_load2(e1.sys, llp + e1.inw + 2, b2w, b3w);
-                }
-            }
-
-            // (1) deferred Phase 3 of cycle t-1, then Phase 1
-            TRACE_EV(has_pend ? 1u : 0u);
-            if (has_pend) { phase3(S, K, c, pend, t - 1, acc); has_pend = false; }
-            TRACE_P1_BEGIN
-            if (MODE == 0u) phase1_ur(S, K, c, t);
-            else phase1_lspd_win<MODE == 2u>(S, K, c, t, wbase, wmask);
-            TRACE_P1_END
-
-            // (2) latch.  Slots 0..3 = link inputs N,S,E,W,
+            // (1) latch.  Slots 0..3 = link inputs N,S,E,W,
             // slot 4 = the injection register.  The occupancy word
             // is consumed (cleared) here.
             const uint32_t ow = own_o + pb * OSTR;
@@ -462,10 +496,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             sts32_if(occ != 0u, ow, 0u);
             uint32_t present = ((occ & 0x01010101u) * 0x01020408u) >> 24;   // byte d -> bit d
             const uint32_t fw = own_f + pb * FSTR;
-            // boundary inputs: poll until each cross-tile slot is complete for
-            // cycle t (word 0 carries stamp t and, for a flit rather than
-            // EMPTY, so do words 1..3); a flit is parked in the node's own
-            // shared slot so all four link inputs are latched alike below
+            // boundary inputs: the polls were issued at the end of the previous
+            // cycle; re-poll until each cross-tile slot is complete for cycle t
+            // (word 0 carries stamp t and, for a flit rather than EMPTY, so do
+            // words 1..3); a flit is parked in the node's own shared slot so
+            // all four link inputs are latched alike below
             if (ext) {
                 bool w0 = true, w1 = e1.port != NOPORT, w2 = ex[2].port != NOPORT, w3 = ex[3].port != NOPORT;
                 uint32_t spins = 0;
@@ -532,18 +567,16 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4], frees)) present |= 16u;
             TRACE_EV(((present & 16u) ? 32u : 0u) | (present ? 64u : 0u) | (ext ? 128u : 0u));
 
-            // (3) first choices (eject at the destination, else x-port, else
+            // (2) first choices (eject at the destination, else x-port, else
             // y-port: PMDR).  If they are pairwise distinct every flit
             // takes its first choice whatever the ranking.  port[k] in
             // `ports` nibble k; inv nibble p = the slot routed to port p
             // (p = 4: the ejected flit)
-            uint32_t seen = 0, coll = 0, ports = 0, inv = 0, bad = 0;
+            uint32_t seen = 0, coll = 0, ports = 0, inv = 0;
 #pragma unroll
             for (uint32_t k = 0; k < 5; ++k) {
                 const uint32_t pk = (present >> k) & 1u;
-                const uint32_t dst = f_dst(f[k]);
-                const uint32_t dy = row_of(S, dst), dx = dst - dy * S.W;
-                const uint32_t fc = dst == c.n ? PX : dx != c.x ? (dx > c.x ? PE : PW) : (dy > c.y ? PS : PN);
+                const uint32_t fc = first_port(f_dst(f[k]), c.n, c.x, c.y, S.W, S.wmagic);
                 const uint32_t b = pk << fc;
                 coll |= seen & b;
                 seen |= b;
@@ -554,7 +587,6 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             // where a flit leaves the tile's registers for good -- at ejection,
             // at a cross-tile hop and at the end of the launch (spill) -- which
             // flags every overflow by the end of the run, as the oracle does
-            (void)bad;
             uint32_t used = seen & 15u;
             bool has_ej = (seen >> PX) & 1u;
             TRACE_EV(coll ? 16u : 0u);
@@ -564,7 +596,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 // link if at its destination and still free, else its first
                 // free productive port, else the first free existing port in
                 // N,S,E,W with age+1 (R3-R6).
-                // The injected flit (age 0, lifetime 0) always ranks last.
+                // The injected flit (lowest age, lifetime 0) always ranks last.
                 uint64_t key[4];
                 uint64_t prefs = 0;
 #pragma unroll
@@ -629,9 +661,10 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 acc.defl += __popc(dm);
             }
             acc.hops += __popc(used);
-            // (4) outputs across the tile boundary first: they are on the
+            // (3) outputs across the tile boundary first: they are on the
             // critical path of the neighbouring tiles.  A routed flit, else an
-            // explicit EMPTY, on every boundary port every cycle.
+            // explicit EMPTY, on every boundary port every cycle.  Then the
+            // polls of the next cycle's boundary inputs.
             if (ext) {
 #pragma unroll
                 for (uint32_t j = 0; j < 4; ++j) {
@@ -647,9 +680,18 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                         ll_store1(e.sys, o, llw(stn, LL_EMPTY));
                     }
                 }
+                if (!last) {
+                    const unsigned long long *const lln = S.ll + (size_t)nb1 * pstride;
+                    ll_load2(e0.sys, lln + e0.inw, a0, a1);
+                    ll_load2(e0.sys, lln + e0.inw + 2, a2, a3);
+                    if (e1.port != NOPORT) {
+                        ll_load2(e1.sys, lln + e1.inw, b0w, b1w);
+                        ll_load2(e1.sys, lln + e1.inw + 2, b2w, b3w);
+                    }
+                }
             }
             TRACE_PUB_DONE
-            // (5) flits that stay in the tile: predicated shared-memory stores
+            // (4) flits that stay in the tile: predicated shared-memory stores
             // into the neighbour's slot opp(p) of cycle t+1
             if (used & intl) {
                 const uint32_t nf = fa + nb1 * FSTR, no = oa + nb1 * OSTR;
@@ -662,46 +704,44 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     sts8_if(go, no + (w >> 16));
                 }
             }
-            // (6) the ejected flit (<= 1): its service runs at the start of
-            // the next cycle (after the tile barrier); prefetch what it reads
+            // (5) Phase 3: the ejected flit (<= 1) is delivered and
+            // serviced now, after this cycle's outputs are out
             if (has_ej) {
                 const Flit g = pick5(f, (inv >> 16) & 15u);
-                // while draining, quiescence is judged at the end of each
-                // cycle, so the service is not deferred there
                 if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32
-                if (DRAIN) phase3(S, K, c, g, t, acc);
-                else { pend = g; has_pend = true; if (MODE != 0u) prefetch_service(S, c, g); }
+                TRACE_EV(1u);
+                phase3(S, K, c, g, t, acc);
             }
-            if (DRAIN) busy = used != 0u || has_pend || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
+            if (DRAIN) busy = used != 0u || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
-        if (windows) {
-            // windows for cycle t+1: idle cores, cores whose wait expires at
-            // t+1, and the deferred service of a reply flit (may complete the
-            // access); also prefetch the set a memory fill installs into
-            bool need = false;
+        TRACE_P3_DONE
+        // (6) Phase 1 of cycle t+1, after the draw windows it needs
+        if (!last) {
+            if (windows) {
+                const bool need = need_window(t + 1);
+                TRACE_EV(__any_sync(FULL, need) ? 8u : 0u);
+                refresh(need, t + 1);
+            }
             if (active) {
-                const uint32_t t1 = stn, mode = core_mode(c.hot);
-                const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ t1) & 0x1FFFFFFFu) == 0u);
-                if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
-                need = (mode == MIDLE || expiring || (has_pend && f_kind(pend) == KRA)) && t1 - wbase >= 32u;
+                const uint32_t h0 = c.hot, q0 = c.qctl;
+                if (MODE == 0u) phase1_ur(S, K, c, t + 1);
+                else phase1_lspd_win<MODE == 2u>(S, K, c, t + 1, wbase, wmask);
+                TRACE_EV((c.hot != h0 ? 2u : 0u) | (c.qctl != q0 ? 4u : 0u));
             }
-            TRACE_EV(__any_sync(FULL, need) ? 8u : 0u);
-            refresh(need, t + 1);
         }
+        TRACE_P1_DONE
         TRACE_END
         // The cycle barrier is a full BAR.SYNC: it orders this cycle's shared-
-        // memory link stores before the next cycle's loads (a reducing barrier,
-        // __syncthreads_or, measurably did not on sm_100a).
+        // memory link stores before the next cycle's loads.
         if (DRAIN && busy) s_busy[cc & 1u] = cc + 1u;
         __syncthreads();
         if (DRAIN && i == 0 && s_busy[cc & 1u] == cc + 1u) atomicAdd(&activity[cc], 1u);
         if (s_abort) break;
     }
 
-    // ---- epilogue: finish the last deferred service, spill state
+    // ---- epilogue: spill state
     const uint64_t tend = t0 + ncyc;
     if (active) {
-        if (has_pend) phase3(S, K, c, pend, tend - 1, acc);
         S.fifo_ctl[c.l] = c.qctl;
         if (MODE != 0u) {
             S.core_hot[c.l] = c.hot;
@@ -817,9 +857,12 @@ bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
 static const void *tiled_fn(uint32_t mode, bool drain, uint32_t feat)
 {
 #define NOC_TD(M, F) (drain ? (const void *)k_tiled<M, true, F> : (const void *)k_tiled<M, false, F>)
-#define NOC_TF(M) (feat == 3u ? NOC_TD(M, 3) : feat == 2u ? NOC_TD(M, 2) : feat == 1u ? NOC_TD(M, 1) : NOC_TD(M, 0))
+#define NOC_TF4(M, B) (feat == 3u + B ? NOC_TD(M, 3 + B) : feat == 2u + B ? NOC_TD(M, 2 + B) : \
+                       feat == 1u + B ? NOC_TD(M, 1 + B) : NOC_TD(M, 0 + B))
+#define NOC_TF(M) (feat >= 4u ? NOC_TF4(M, 4) : NOC_TF4(M, 0))
     return mode == 2u ? NOC_TF(2) : mode == 1u ? NOC_TF(1) : NOC_TF(0);
 #undef NOC_TF
+#undef NOC_TF4
 #undef NOC_TD
 }
 
@@ -867,7 +910,7 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
     const bool dr = activity != nullptr;
     const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr,
-                              P.d[0].route | (P.d[0].inject_mode << 1));
+                              P.d[0].route | (P.d[0].inject_mode << 1) | (P.nbands > 1 ? 4u : 0u));
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }
 

@@ -49,6 +49,8 @@ print("last-warp arrival (clk): median %d  p90 %d ; barrier release gap median %
 print("warp compute time (clk): median %d  mean %d  p90 %d  p99 %d" % (
     np.median(arr), arr.mean(), np.percentile(arr, 90), np.percentile(arr, 99)))
 names = ["phase3", "p1-state", "p1-enq", "refresh", "conflict", "inject", "flits", "boundary"]
+# per-warp offsets (clk from the warp's cycle start): ext inputs complete, boundary
+# outputs published, Phase 3 done, Phase 1 of the next cycle done, barrier arrival
 e3 = ev.reshape(TRACE_CYC, grid, wpc)
 print("%-10s %8s %10s %10s %12s" % ("event", "warps%", "time(with)", "time(w/o)", "in last warp%"))
 lw = fin.argmax(axis=2)
@@ -68,7 +70,7 @@ for nm, msk in (("boundary", bnd), ("interior", ~bnd)):
     if not msk.any():
         continue
     q = lambda a: "%5d %5d %5d" % (np.percentile(a[msk], 50), np.percentile(a[msk], 90), a[msk].mean())
-    print("%s warps (p50 p90 mean clk from cycle start): phase3 done %s | phase1 done %s | ext done %s | "
-          "published %s | barrier %s" % (nm, q(p3w.reshape(arr.shape)), q(p1w.reshape(arr.shape)),
-                                          q(bx), q(pubw.reshape(arr.shape)), q(arr)))
+    print("%s warps (p50 p90 mean clk from cycle start): ext done %s | published %s | phase3 done %s | "
+          "phase1 done %s | barrier %s" % (nm, q(bx), q(pubw.reshape(arr.shape)), q(p3w.reshape(arr.shape)),
+                                          q(p1w.reshape(arr.shape)), q(arr)))
 print("last warp is a boundary warp in %.1f%% of CTA-cycles" % (100 * ((lastev >> 7) & 1).mean()))
