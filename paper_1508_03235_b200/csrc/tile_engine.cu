@@ -448,6 +448,22 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
         return (mode == MIDLE || expiring) && (uint32_t)tn - wbase >= 32u;
     };
+    // LSPD with draw windows: Phase 1 of a node has work only at its next due
+    // cycle `wake` -- its timer expiry (L2 hit, memory fill, L1 miss), the next
+    // firing draw of its window while IDLE, or the window's end (refresh) --
+    // or in the cycle after a Phase-3 state change.  Other cycles skip it.
+    uint32_t wake = 0;
+    auto wake_from = [&](uint32_t tc) -> uint32_t {   // next due cycle after tc
+        const uint32_t mode = core_mode(c.hot);
+        if (mode == MIDLE) {
+            const uint32_t k = tc + 1u - wbase;
+            if (k >= 32u) return tc + 1u;
+            const uint32_t m = wmask >> k;
+            return m ? tc + (uint32_t)__ffs(m) : wbase + 32u;
+        }
+        if (mode == MWAITDIR || mode == MWAITDATA) return tc;    // woken by Phase 3 only
+        return tc + ((c.hot - tc) & 0x1FFFFFFFu);                // the timer (ready mod 2^29)
+    };
     const uint32_t pstride = 16u * S.nloc;
     Sink K{scnt, shist, true};
     Acc acc = {0, 0, 0, 0};
@@ -476,6 +492,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     if (active) {
         if (MODE == 0u) phase1_ur(S, K, c, t0);
         else phase1_lspd_win<MODE == 2u>(S, K, c, t0, wbase, wmask);
+        if (windows) wake = wake_from((uint32_t)t0);
     }
     __syncthreads();
 
@@ -711,6 +728,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32
                 TRACE_EV(1u);
                 phase3(S, K, c, g, t, acc);
+                if (windows) wake = wake_from(st);
             }
             if (DRAIN) busy = used != 0u || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
@@ -718,11 +736,22 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         // (6) Phase 1 of cycle t+1, after the draw windows it needs
         if (!last) {
             if (windows) {
-                const bool need = need_window(t + 1);
-                TRACE_EV(__any_sync(FULL, need) ? 8u : 0u);
-                refresh(need, t + 1);
-            }
-            if (active) {
+                const bool due = active && stn == wake;
+                const bool need = due && stn - wbase >= 32u;
+                // the set a memory fill installs into one cycle ahead (L1 prefetch)
+                if (active && stn + 1u == wake && core_mode(c.hot) == MMEMWAIT && (c.cold.w & 1u))
+                    prefetch_l1(set_ptr(S, c, c.cold.z));
+                if (__any_sync(FULL, need)) {
+                    TRACE_EV(8u);
+                    refresh(need, t + 1);
+                }
+                if (due) {
+                    const uint32_t h0 = c.hot, q0 = c.qctl;
+                    phase1_lspd_win<MODE == 2u>(S, K, c, t + 1, wbase, wmask);
+                    wake = wake_from(stn);
+                    TRACE_EV((c.hot != h0 ? 2u : 0u) | (c.qctl != q0 ? 4u : 0u));
+                }
+            } else if (active) {
                 const uint32_t h0 = c.hot, q0 = c.qctl;
                 if (MODE == 0u) phase1_ur(S, K, c, t + 1);
                 else phase1_lspd_win<MODE == 2u>(S, K, c, t + 1, wbase, wmask);
