@@ -18,6 +18,7 @@ struct DevSet {
     Dev d[MAX_BANDS];
     uint32_t nbands;
     uint32_t tile0[MAX_BANDS + 1];   // first CTA of each band
+    uint32_t general;                // several bands or ranks: band lookup and system-scope band-edge links
 };
 
 // TILED engine (tile_engine.cu): tiled_plan picks the tiling of one band

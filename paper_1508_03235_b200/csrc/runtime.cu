@@ -417,6 +417,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         const uint32_t per_sm = four ? TILE4_MIN_BLOCKS : TILE_MIN_BLOCKS;
         const uint32_t budget = std::max<uint32_t>(1u, (uint32_t)s->sm_count * per_sm / (uint32_t)s->nb);
         s->set.nbands = (uint32_t)s->nb;
+        s->set.general = s->nb > 1 || s->world > 1;
         s->set.tile0[0] = 0;
         for (int k = 0; k < s->nb && ok; ++k) {
             uint32_t tiles = 0, npk = 0;
@@ -428,7 +429,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         cudaError_t ce = cudaErrorInvalidConfiguration;
         if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
                           : tiled_prepare(cfg->mode == NOC_MODE_LSPD && cfg->l1_sets ? 2u : cfg->mode,
-                                          cfg->route | (cfg->inject_mode << 1) | (s->nb > 1 ? 4u : 0u),
+                                          cfg->route | (cfg->inject_mode << 1) | (s->nb > 1 || s->world > 1 ? 4u : 0u),
                                           cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {
             s->engine = cand;
