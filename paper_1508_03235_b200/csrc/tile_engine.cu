@@ -274,7 +274,7 @@ struct ExtIn {
     uint32_t port;   // N, S, E or W; NOPORT if none
     uint32_t inw;    // LL word index (parity 0) of this node's input slot
     uint32_t outw;   // LL word index (parity 0) of the receiver's slot for output `port`
-    bool sys;        // crosses the band edge (system scope; general kernel only)
+    bool sys;        // crosses the band edge (system scope)
 };
 constexpr uint32_t NOPORT = 8u;
 
@@ -289,11 +289,10 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 {
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     // this CTA's band and tile
-    // FEAT bit 2: several bands in this launch (virtual bands) or several
-    // ranks (band edges at system scope).  Without it the parameters are read
-    // at constant offsets (constant-bank operands of the instructions
-    // themselves) instead of indexed constant loads that the register-starved
-    // loop would otherwise re-issue every cycle, and no link is system scope
+    // FEAT bit 2: several bands in this launch (virtual bands).  With one band
+    // the parameters are read at constant offsets (constant-bank operands of
+    // the instructions themselves) instead of indexed constant loads that the
+    // register-starved loop would otherwise re-issue every cycle
     uint32_t band = 0;
     if (FEAT & 4u)
         while (band + 1 < P.nbands && blockIdx.x >= P.tile0[band + 1]) ++band;
@@ -482,11 +481,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0w = 0, b1w = 0, b2w = 0, b3w = 0;
     if (active && ext) {
         const unsigned long long *const llp = S.ll + (size_t)b0 * pstride;
-        ll_load2(((FEAT & 4u) && e0.sys), llp + e0.inw, a0, a1);
-        ll_load2(((FEAT & 4u) && e0.sys), llp + e0.inw + 2, a2, a3);
+        ll_load2(e0.sys, llp + e0.inw, a0, a1);
+        ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
         if (e1.port != NOPORT) {
-            ll_load2(((FEAT & 4u) && e1.sys), llp + e1.inw, b0w, b1w);
-            ll_load2(((FEAT & 4u) && e1.sys), llp + e1.inw + 2, b2w, b3w);
+            ll_load2(e1.sys, llp + e1.inw, b0w, b1w);
+            ll_load2(e1.sys, llp + e1.inw + 2, b2w, b3w);
         }
     }
     if (windows) refresh(need_window(t0), t0);
@@ -514,51 +513,30 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             sts32_if(occ != 0u, ow, 0u);
             uint32_t present = ((occ & 0x01010101u) * 0x01020408u) >> 24;   // byte d -> bit d
             const uint32_t fw = own_f + pb * FSTR;
-            // the internal inputs and their first choices (eject at the
-            // destination, else x-port, else y-port: PMDR), taken
-            // before the boundary inputs are awaited: only the boundary
-            // inputs' own first choices remain on a ring node's path from
-            // their arrival to the publication of its boundary outputs.
-            // Nibble k of `ports` = first choice of slot k.
-            Flit f[5];
-#pragma unroll
-            for (uint32_t d = 0; d < 5; ++d) f[d] = Flit{0, 0, 0, 0};
-#pragma unroll
-            for (uint32_t d = 0; d < 4; ++d) lds128_if((present >> d) & 1u, fw + d * 16u * np, f[d]);
-            uint32_t ports = 0;
-#pragma unroll
-            for (uint32_t d = 0; d < 4; ++d) ports |= first_port(f_dst(f[d]), c.n, c.x, c.y, S.W, S.wmagic) << (4u * d);
             // boundary inputs: the polls were issued at the end of the previous
             // cycle; re-poll until each cross-tile slot is complete for cycle t
             // (word 0 carries stamp t and, for a flit rather than EMPTY, so do
-            // words 1..3); a flit is parked in the node's own shared slot and
-            // re-read below, its first choice is taken on arrival
-            uint32_t xin = 0;   // boundary slots that received a flit
+            // words 1..3); a flit is parked in the node's own shared slot so
+            // all four link inputs are latched alike below
             if (ext) {
                 bool w0 = true, w1 = e1.port != NOPORT, w2 = ex[2].port != NOPORT, w3 = ex[3].port != NOPORT;
                 uint32_t spins = 0;
-                auto arrive = [&](const ExtIn &e, uint32_t x, unsigned long long y, unsigned long long z,
-                                  unsigned long long w) {
-                    sts128_if(true, fw + e.port * 16u * np,
-                              Flit{x, (uint32_t)(y >> 32), (uint32_t)(z >> 32), (uint32_t)(w >> 32)});
-                    xin |= 1u << e.port;
-                    ports = (ports & ~(15u << (4u * e.port))) |
-                            first_port(x & NODE_MASK, c.n, c.x, c.y, S.W, S.wmagic) << (4u * e.port);
-                };
                 while (true) {
 #pragma unroll
                     for (uint32_t j = 2; j < 4; ++j) {
                         bool &wj = j == 2 ? w2 : w3;
                         if (!wj) continue;
                         unsigned long long c0, c1, c2, c3;
-                        ll_load2(((FEAT & 4u) && ex[j].sys), llp + ex[j].inw, c0, c1);
-                        ll_load2(((FEAT & 4u) && ex[j].sys), llp + ex[j].inw + 2, c2, c3);
+                        ll_load2(ex[j].sys, llp + ex[j].inw, c0, c1);
+                        ll_load2(ex[j].sys, llp + ex[j].inw + 2, c2, c3);
                         if ((uint32_t)c0 != st) continue;
                         const uint32_t x = (uint32_t)(c0 >> 32);
                         if (x == LL_EMPTY) wj = false;
                         else if ((uint32_t)c1 == st && (uint32_t)c2 == st && (uint32_t)c3 == st) {
                             wj = false;
-                            arrive(ex[j], x, c1, c2, c3);
+                            sts128_if(true, fw + ex[j].port * 16u * np,
+                                      Flit{x, (uint32_t)(c1 >> 32), (uint32_t)(c2 >> 32), (uint32_t)(c3 >> 32)});
+                            present |= 1u << ex[j].port;
                         }
                     }
                     if (w0 && (uint32_t)a0 == st) {
@@ -566,7 +544,9 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                         if (x == LL_EMPTY) w0 = false;
                         else if ((uint32_t)a1 == st && (uint32_t)a2 == st && (uint32_t)a3 == st) {
                             w0 = false;
-                            arrive(e0, x, a1, a2, a3);
+                            sts128_if(true, fw + e0.port * 16u * np,
+                                      Flit{x, (uint32_t)(a1 >> 32), (uint32_t)(a2 >> 32), (uint32_t)(a3 >> 32)});
+                            present |= 1u << e0.port;
                         }
                     }
                     if (w1 && (uint32_t)b0w == st) {
@@ -574,46 +554,50 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                         if (x == LL_EMPTY) w1 = false;
                         else if ((uint32_t)b1w == st && (uint32_t)b2w == st && (uint32_t)b3w == st) {
                             w1 = false;
-                            arrive(e1, x, b1w, b2w, b3w);
+                            sts128_if(true, fw + e1.port * 16u * np,
+                                      Flit{x, (uint32_t)(b1w >> 32), (uint32_t)(b2w >> 32), (uint32_t)(b3w >> 32)});
+                            present |= 1u << e1.port;
                         }
                     }
                     if (!(w0 || w1 || w2 || w3)) break;
                     if (++spins > (1u << 22)) { atomicOr(S.err, 0x80000000u); s_abort = 1; break; }
                     if (w0) {
-                        ll_load2(((FEAT & 4u) && e0.sys), llp + e0.inw, a0, a1);
-                        ll_load2(((FEAT & 4u) && e0.sys), llp + e0.inw + 2, a2, a3);
+                        ll_load2(e0.sys, llp + e0.inw, a0, a1);
+                        ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
                     }
                     if (w1) {
-                        ll_load2(((FEAT & 4u) && e1.sys), llp + e1.inw, b0w, b1w);
-                        ll_load2(((FEAT & 4u) && e1.sys), llp + e1.inw + 2, b2w, b3w);
+                        ll_load2(e1.sys, llp + e1.inw, b0w, b1w);
+                        ll_load2(e1.sys, llp + e1.inw + 2, b2w, b3w);
                     }
                 }
-#pragma unroll
-                for (uint32_t d = 0; d < 4; ++d) lds128_if((xin >> d) & 1u, fw + d * 16u * np, f[d]);
-                present |= xin;
             }
             TRACE_EXT_DONE
+            Flit f[5];
+#pragma unroll
+            for (uint32_t d = 0; d < 5; ++d) f[d] = Flit{0, 0, 0, 0};
+#pragma unroll
+            for (uint32_t d = 0; d < 4; ++d) lds128_if((present >> d) & 1u, fw + d * 16u * np, f[d]);
             uint32_t frees = 0u;   // NEXT-f4 injection mode (R43): an ejecting flit frees its port
             if (FEAT & 2u)
 #pragma unroll
-                for (uint32_t d = 0; d < 4; ++d) frees |= ((present >> d) & 1u) && ((ports >> (4u * d)) & 15u) == PX;
-            if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4], frees)) {
-                present |= 16u;
-                ports |= first_port(f_dst(f[4]), c.n, c.x, c.y, S.W, S.wmagic) << 16;
-            }
+                for (uint32_t d = 0; d < 4; ++d) frees |= ((present >> d) & 1u) && f_dst(f[d]) == c.n;
+            if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4], frees)) present |= 16u;
             TRACE_EV(((present & 16u) ? 32u : 0u) | (present ? 64u : 0u) | (ext ? 128u : 0u));
 
-            // (2) if the first choices are pairwise distinct every flit takes
-            // its first choice whatever the ranking.  inv nibble p = the slot
-            // routed to port p (p = 4: the ejected flit)
-            uint32_t seen = 0, coll = 0, inv = 0;
+            // (2) first choices (eject at the destination, else x-port, else
+            // y-port: PMDR).  If they are pairwise distinct every flit
+            // takes its first choice whatever the ranking.  port[k] in
+            // `ports` nibble k; inv nibble p = the slot routed to port p
+            // (p = 4: the ejected flit)
+            uint32_t seen = 0, coll = 0, ports = 0, inv = 0;
 #pragma unroll
             for (uint32_t k = 0; k < 5; ++k) {
                 const uint32_t pk = (present >> k) & 1u;
-                const uint32_t fc = (ports >> (4u * k)) & 15u;
+                const uint32_t fc = first_port(f_dst(f[k]), c.n, c.x, c.y, S.W, S.wmagic);
                 const uint32_t b = pk << fc;
                 coll |= seen & b;
                 seen |= b;
+                ports |= fc << (4u * k);
                 inv |= pk ? k << (4u * fc) : 0u;
             }
             // R32 lifetime limit: a flit's lifetime only grows, so it is checked
@@ -703,23 +687,23 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 for (uint32_t j = 0; j < 4; ++j) {
                     const ExtIn &e = ex[j];
                     if (e.port == NOPORT) continue;
-                    unsigned long long *o = ll_out(S, ((FEAT & 4u) && e.sys), e.port, nb1, pstride) + e.outw;
+                    unsigned long long *o = ll_out(S, e.sys, e.port, nb1, pstride) + e.outw;
                     if ((used >> e.port) & 1u) {
                         const Flit g = pick5(f, (inv >> (4u * e.port)) & 15u);
                         if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32, at a cross-tile hop
-                        ll_store2(((FEAT & 4u) && e.sys), o + 2, llw(stn, g.z), llw(stn, g.w));
-                        ll_store2(((FEAT & 4u) && e.sys), o, llw(stn, g.x), llw(stn, g.y));
+                        ll_store2(e.sys, o + 2, llw(stn, g.z), llw(stn, g.w));
+                        ll_store2(e.sys, o, llw(stn, g.x), llw(stn, g.y));
                     } else {
-                        ll_store1(((FEAT & 4u) && e.sys), o, llw(stn, LL_EMPTY));
+                        ll_store1(e.sys, o, llw(stn, LL_EMPTY));
                     }
                 }
                 if (!last) {
                     const unsigned long long *const lln = S.ll + (size_t)nb1 * pstride;
-                    ll_load2(((FEAT & 4u) && e0.sys), lln + e0.inw, a0, a1);
-                    ll_load2(((FEAT & 4u) && e0.sys), lln + e0.inw + 2, a2, a3);
+                    ll_load2(e0.sys, lln + e0.inw, a0, a1);
+                    ll_load2(e0.sys, lln + e0.inw + 2, a2, a3);
                     if (e1.port != NOPORT) {
-                        ll_load2(((FEAT & 4u) && e1.sys), lln + e1.inw, b0w, b1w);
-                        ll_load2(((FEAT & 4u) && e1.sys), lln + e1.inw + 2, b2w, b3w);
+                        ll_load2(e1.sys, lln + e1.inw, b0w, b1w);
+                        ll_load2(e1.sys, lln + e1.inw + 2, b2w, b3w);
                     }
                 }
             }
@@ -871,7 +855,12 @@ bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
 {
     uint64_t best_tn = ~0ull, best_per = ~0ull;
     uint32_t bx = 0, by = 0;
-    for (uint32_t tx = 1; tx <= S.W && tx <= tiles_budget; ++tx) {
+    // a band that fits one CTA runs as ONE tile: no cross-tile exchange at all,
+    // the cycle barrier is the only synchronisation (measured: a cycle with an
+    // exchange costs 4-6x one without, whatever the tile size, DESIGN 6.4)
+    const bool one = (uint64_t)S.W * S.rows <= TILE_BLOCK_MAX && !getenv("NOCSIM_TILING");
+    if (one) { bx = by = 1; best_tn = (uint64_t)S.W * S.rows; }
+    for (uint32_t tx = 1; !one && tx <= S.W && tx <= tiles_budget; ++tx) {
         for (uint32_t ty = 1; ty <= S.rows && (uint64_t)tx * ty <= tiles_budget; ++ty) {
             uint64_t tw = (S.W + tx - 1) / tx, th = (S.rows + ty - 1) / ty;
             uint64_t tn = tw * th, per = tw + th;

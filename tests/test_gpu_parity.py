@@ -203,6 +203,23 @@ def test_tiled_odd_tilings(w, h, engine):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("tiling", ["3x4", "13x1", "1x11"])
+def test_small_mesh_forced_tilings(tiling, monkeypatch):
+    """A mesh that fits one CTA runs as one tile (no cross-tile exchange);
+    the NOCSIM_TILING hook still forces a multi-tile layout on it, which must
+    give the same results (ragged, 1-wide and 1-tall tiles)."""
+    cfg = W.make(mesh_w=13, mesh_h=11, mode=W.MODE_LSPD, lam=0.3, sendq_cap=32, l2_sets=4, mem_lat=20)
+    g1 = nb.NocSim(cfg, engine=nb.ENGINE_TILED)
+    assert g1.info()["grid"] == 1
+    monkeypatch.setenv("NOCSIM_TILING", tiling)
+    g, o = both(cfg, 1500, nb.ENGINE_TILED)
+    a, b = (int(v) for v in tiling.split("x"))
+    assert g.info()["grid"] == a * b
+    assert_same(g, o)
+    g1.run(1500)
+    assert g1.state_hash() == o.state_hash()
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
 def test_launch_boundaries(engine, mode):
