@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define NOC_SIM_ABI_VERSION 3u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base */
+#define NOC_SIM_ABI_VERSION 4u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base; 4: band_streams */
 
 /* error codes */
 #define NOC_OK          0
@@ -128,7 +128,15 @@ typedef struct noc_sim_config {
                                   <= 65535.  Shifts every age equally (ranking
                                   unchanged) so tests reach ages >= 2048 and the
                                   R32 age limit (NOC_EOVERFLOW)                  */
-    uint32_t reserved[3];      /* must be 0                                        */
+    uint32_t band_streams;     /* bands > 1 with the TILED engine: 1 = "virtual
+                                  ranks": every band is advanced by its own
+                                  launches on its own stream, with the
+                                  multi-process sequence per launch (slot
+                                  refresh, a cross-band barrier, the band's
+                                  cooperative launch, a barrier) and events
+                                  in place of the NCCL barrier; 0 = all bands
+                                  in one launch.  Results are identical     */
+    uint32_t reserved[2];      /* must be 0                                        */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list

@@ -49,7 +49,8 @@ class noc_sim_config(C.Structure):
         ("engine", C.c_uint32), ("nccl_id", C.c_uint8 * 128), ("bands", C.c_uint32),
         ("route", C.c_uint32), ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
-        ("inject_mode", C.c_uint32), ("age_base", C.c_uint32), ("reserved", C.c_uint32 * 3),
+        ("inject_mode", C.c_uint32), ("age_base", C.c_uint32), ("band_streams", C.c_uint32),
+        ("reserved", C.c_uint32 * 2),
     ]
 
 
@@ -96,7 +97,7 @@ def lib():
         L.noc_sim_destroy.argtypes = [P]
         L.noc_sim_last_error.restype = C.c_char_p
         L.noc_sim_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
-        if L.noc_sim_abi_version() != 3:   # include/noc_sim.h NOC_SIM_ABI_VERSION
+        if L.noc_sim_abi_version() != 4:   # include/noc_sim.h NOC_SIM_ABI_VERSION
             raise NocSimError(NOC_EINVAL, "ABI version mismatch")
         _lib = L
     return _lib

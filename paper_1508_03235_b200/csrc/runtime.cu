@@ -77,6 +77,12 @@ struct noc_sim {
     int world = 1, rank = 0;
     ncclComm_t comm = nullptr;
     std::vector<void *> ipc_opened;
+    // virtual ranks (band_streams): one stream, launch set and events per band
+    int split = 0;
+    cudaStream_t bst[MAX_BANDS] = {};
+    cudaEvent_t bev[MAX_BANDS] = {};
+    cudaEvent_t mev = nullptr;
+    DevSet bset[MAX_BANDS];
     std::vector<void *> allocs;
     uint64_t bytes = 0, loc_bytes = 0;
     uint64_t launches = 0;
@@ -134,6 +140,10 @@ static int validate(const noc_sim_config *c)
         if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->inject_mode > 1) return fail(NOC_EINVAL, "inject_mode out of range");
     if (c->age_base > AGE_MAX) return fail(NOC_EINVAL, "age_base > 65535 (R32)");
+    if (c->band_streams > 1) return fail(NOC_EINVAL, "band_streams must be 0 or 1");
+    if (c->band_streams && (c->bands < 2 || c->world_size > 1 ||
+                            (c->engine != NOC_ENGINE_TILED && c->engine != NOC_ENGINE_AUTO)))
+        return fail(NOC_EINVAL, "band_streams needs bands >= 2 in one process and the TILED engine");
     if (c->inject_mode && c->engine == NOC_ENGINE_TILED4)
         return fail(NOC_EINVAL, "inject_mode 1 needs five flit lanes per router: not with the TILED4 engine");
     if (c->mode == NOC_MODE_LSPD && c->l1_sets &&
@@ -161,6 +171,11 @@ extern "C" void noc_sim_destroy(noc_sim *s)
     for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
     if (s->comm) ncclCommDestroy(s->comm);
     for (void *p : s->allocs) cudaFree(p);
+    for (int k = 0; k < MAX_BANDS; ++k) {
+        if (s->bst[k]) { cudaStreamSynchronize(s->bst[k]); cudaStreamDestroy(s->bst[k]); }
+        if (s->bev[k]) cudaEventDestroy(s->bev[k]);
+    }
+    if (s->mev) cudaEventDestroy(s->mev);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->stream) cudaStreamDestroy(s->stream);
@@ -457,6 +472,25 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
             if (launch_ll_reset(s->D[k], 0, s->stream) != cudaSuccess) return bail(fail(NOC_ECUDA, "ll reset failed"));
             s->set.d[k] = s->D[k];
         }
+        if (cfg->band_streams) {
+            if (s->engine != NOC_ENGINE_TILED) return bail(fail(NOC_EINVAL, "band_streams needs the TILED engine"));
+            // each band alone in its launch (like one rank's band), on its own stream
+            s->split = 1;
+            if (cudaEventCreateWithFlags(&s->mev, cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(NOC_ECUDA, "event creation failed"));
+            for (int k = 0; k < s->nb; ++k) {
+                if (cudaStreamCreateWithFlags(&s->bst[k], cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&s->bev[k], cudaEventDisableTiming) != cudaSuccess)
+                    return bail(fail(NOC_ECUDA, "band stream creation failed"));
+                DevSet &B = s->bset[k];
+                B = s->set;
+                B.d[0] = s->D[k];
+                B.nbands = 1;
+                B.tile0[0] = 0;
+                B.tile0[1] = s->set.tile0[k + 1] - s->set.tile0[k];
+                B.general = 1;
+            }
+        }
     }
     if (s->engine == NOC_ENGINE_PERSIST) {
         // each band: its CTAs, nodes per CTA and progress counters; then the
@@ -531,7 +565,37 @@ static void set_gen(noc_sim *s, uint32_t gen)
 static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
 {
     cudaError_t e;
-    if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
+    if (s->split) {
+        // virtual ranks: per band, the launch sequence of one rank (DESIGN 8)
+        // -- refresh its boundary slots, barrier with the other bands, its own
+        // cooperative launch, barrier -- each band on its own stream; the
+        // barriers are events every band stream waits for
+        auto barrier = [&]() -> int {
+            for (int b = 0; b < s->nb; ++b) CU(cudaEventRecord(s->bev[b], s->bst[b]));
+            for (int b = 0; b < s->nb; ++b)
+                for (int j = 0; j < s->nb; ++j)
+                    if (j != b) CU(cudaStreamWaitEvent(s->bst[b], s->bev[j], 0));
+            return NOC_OK;
+        };
+        CU(cudaEventRecord(s->mev, s->stream));
+        for (int b = 0; b < s->nb; ++b) CU(cudaStreamWaitEvent(s->bst[b], s->mev, 0));
+        uint64_t done = 0;
+        int rc;
+        while (done < n) {
+            uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
+            for (int b = 0; b < s->nb; ++b) CU(launch_ll_refresh(s->D[b], s->t + done, s->bst[b]));
+            if ((rc = barrier())) return rc;
+            uint32_t *act = activity ? activity + done : nullptr;
+            for (int b = 0; b < s->nb; ++b) {
+                e = launch_tiled(s->bset[b], s->t + done, k, s->t_tpad, s->t_smem_hist, act, s->bst[b]);
+                if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("tiled band launch: ") + cudaGetErrorString(e));
+            }
+            if ((rc = barrier())) return rc;
+            done += k;
+            s->launches += 1;
+        }
+        for (int b = 0; b < s->nb; ++b) CU(cudaStreamWaitEvent(s->stream, s->bev[b], 0));
+    } else if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);

@@ -70,7 +70,8 @@ def test_struct_layouts_match_header():
 @pytest.mark.parametrize("bad", [
     dict(mesh_w=1), dict(mesh_h=4096), dict(sendq_cap=3), dict(hist_bins=0), dict(nfl_ra=9),
     dict(mode=W.MODE_LSPD, priv_tags=128), dict(mode=W.MODE_LSPD, l2_ways=17),
-    dict(mode=W.MODE_LSPD, mem_lat=0), dict(mode=2),
+    dict(mode=W.MODE_LSPD, mem_lat=0), dict(mode=2), dict(age_base=65536), dict(band_streams=1),
+    dict(band_streams=2),
 ])
 def test_invalid_configs_rejected_before_device(bad):
     cfg = W.make(**bad)

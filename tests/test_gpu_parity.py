@@ -269,6 +269,40 @@ def test_virtual_bands_match_oracle(bands, mode, engine):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("bands", [2, 3, 4])
+@pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
+def test_virtual_ranks_band_streams(bands, mode):
+    """"Virtual ranks" (band_streams): each band advanced by its own launches
+    on its own stream with the multi-process launch sequence (refresh,
+    cross-band barrier, launch, barrier; events instead of NCCL) -- the
+    world_size > 1 host logic on one GPU -- bit-exact against the oracle,
+    across many launch boundaries and a drain."""
+    if mode == W.MODE_UR:
+        cfg = W.make(mesh_w=40, mesh_h=37, mode=W.MODE_UR, lam=0.3, band_streams=1)
+    else:
+        cfg = W.lspd(40, 37, lam=0.2, band_streams=1)
+    g = nb.NocSim(cfg, bands=bands, engine=nb.ENGINE_TILED)
+    o = Oracle(cfg)
+    for k in (1, 5, 250, 744, 1000):
+        g.run(k)
+        o.run(k)
+    assert g.drain(20000) == o.drain(20000)
+    g.run(300)
+    o.run(300)
+    assert_same(g, o)
+
+
+def test_virtual_ranks_c3():
+    """The bench mesh as 2 virtual ranks, in the bench's launch split."""
+    cfg = W.c3(band_streams=1)
+    g = nb.NocSim(cfg, bands=2, engine=nb.ENGINE_TILED)
+    o = Oracle(cfg)
+    for _ in range(2):
+        g.run(500)
+        o.run(500)
+        assert_same(g, o)
+
+
 def test_virtual_bands_c3():
     cfg = W.c3()
     g = nb.NocSim(cfg, bands=2)
