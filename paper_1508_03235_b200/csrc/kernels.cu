@@ -377,6 +377,12 @@ cudaError_t launch_persist(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t
     size_t smem = persist_smem_bytes(P.d[0], smem_hist != 0);
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&pbase, (void *)&smem_hist, (void *)&activity};
     const void *fn = P.d[0].mode == 1u ? (const void *)k_persist<1> : (const void *)k_persist<0>;
+    // the dynamic shared-memory limit is a per-function (process-wide)
+    // attribute: another handle of a different size may have lowered it
+    {
+        const cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return ea;
+    }
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(PERSIST_BLOCK), args, smem, st);
 }
 

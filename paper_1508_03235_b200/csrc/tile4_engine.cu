@@ -507,6 +507,12 @@ cudaError_t launch_tiled4(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t 
     const void *fn = P.d[0].mode == 1u
                          ? (dr ? (const void *)t4::k_tiled4<1, true> : (const void *)t4::k_tiled4<1, false>)
                          : (dr ? (const void *)t4::k_tiled4<0, true> : (const void *)t4::k_tiled4<0, false>);
+    // the dynamic shared-memory limit is a per-function (process-wide)
+    // attribute: another handle of a different size may have lowered it
+    {
+        const cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return ea;
+    }
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(4u * np), args, smem, st);
 }
 

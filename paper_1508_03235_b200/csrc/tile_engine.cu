@@ -945,6 +945,12 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     const bool dr = activity != nullptr;
     const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr,
                               P.d[0].route | (P.d[0].inject_mode << 1) | (P.general ? 4u : 0u));
+    // the dynamic shared-memory limit is a per-function (process-wide)
+    // attribute: another handle of a different size may have lowered it
+    {
+        const cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return ea;
+    }
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }
 
