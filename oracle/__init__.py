@@ -29,6 +29,8 @@ COUNTER_NAMES = (
 )
 KIND_NAMES = ("probe", "da", "dr", "ndr", "rq", "ra", "trap", "ev")
 L1_COUNTER_NAMES = ("l1_hits", "l1_misses", "wb_sent", "wb_received")   # NEXT-f1 (R42)
+MIG_COUNTER_NAMES = ("mig_requests", "mig_nacks", "migrations", "mig_installs",
+                     "dir_updates", "invalidations", "redirections", "rr_received")   # NEXT-f2
 
 MODE_UR, MODE_LSPD = 0, 1
 PRIO_DEFLECT, PRIO_OLDEST = 0, 1
@@ -61,12 +63,13 @@ class _Config(C.Structure):
         ("dir_mode", C.c_uint32), ("dir_node", C.c_uint32),
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
         ("inject_mode", C.c_uint32), ("age_base", C.c_uint32),
+        ("mig_hist", C.c_uint32), ("nfl_b2", C.c_uint32),
     ]
 
 
 class _Counters(C.Structure):
     _fields_ = [("cycle", C.c_int64)] + [(n, C.c_int64) for n in COUNTER_NAMES] + [
-        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES]
+        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES]
 
 
 _lib = None
@@ -110,6 +113,12 @@ def lib():
         L.orc_script_used.restype = C.c_int64
         L.orc_gen.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint64)]
         L.orc_poke.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64]
+        L.orc_l2_mig.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.orc_loc_mig.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.orc_mig_target.argtypes = [C.POINTER(C.c_uint32), C.c_uint32, C.c_uint32]
+        L.orc_l2_hist.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]
+        L.orc_migrx.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]
+        L.orc_mig_target.restype = C.c_uint32
         _lib = L
     return _lib
 
@@ -204,7 +213,7 @@ class Oracle:
             d[n] = getattr(cnt, n)
         for i, k in enumerate(KIND_NAMES):
             d["drops_" + k] = cnt.drops[i]
-        for n in L1_COUNTER_NAMES:
+        for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES:
             d[n] = getattr(cnt, n)
         return d, list(hl), list(hd), list(ha)
 
@@ -277,3 +286,34 @@ class Oracle:
     def poke(self, field, n=0, i=0, j=0, value=1):
         """Test-only single-field mutation (fields listed at orc_poke)."""
         _check(lib().orc_poke(self._h, field, n, i, j, value & 0xFFFFFFFFFFFFFFFF))
+
+    def l2_mig(self, n, s_, w):
+        """NEXT-f2: (mstate, mtarget, hcount) of L2 line (n, set, way); mstate 0 NORMAL,
+        1 MIGREQ, 2 MIGSENT, 3 FWD (forwarding ghost)."""
+        o = (C.c_uint64 * 3)()
+        _check(lib().orc_l2_mig(self._h, n, s_, w, o))
+        return tuple(int(x) for x in o)
+
+    def l2_hist(self, n, s_, w):
+        """NEXT-f2: accessor history of L2 line (n, set, way), oldest first."""
+        o = (C.c_uint32 * 16)()
+        k = lib().orc_l2_hist(self._h, n, s_, w, o)
+        return list(o[:max(k, 0)])
+
+    def migrx(self, n, k):
+        o = (C.c_uint64 * 3)()
+        _check(lib().orc_migrx(self._h, n, k, o))
+        return tuple(int(x) for x in o)
+
+    def loc_mig(self, T):
+        o = (C.c_uint64 * 2)()
+        _check(lib().orc_loc_mig(self._h, T, o))
+        return tuple(int(x) for x in o)
+
+
+def mig_target(history, holder):
+    """NEXT-f2 migration decision (R46) on an accessor history (oldest first):
+    the target node or None."""
+    arr = (C.c_uint32 * max(1, len(history)))(*history)
+    r = lib().orc_mig_target(arr, len(history), holder)
+    return None if r == 0xFFFFFFFF else int(r)

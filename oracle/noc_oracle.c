@@ -25,6 +25,12 @@
 enum { DIR_N = 0, DIR_S = 1, DIR_E = 2, DIR_W = 3, PORT_EJECT = 4 };
 /* message kinds: Table I + readings R16, R18, R13 */
 enum { K_PROBE = 0, K_DA = 1, K_DR = 2, K_NDR = 3, K_RQ = 4, K_RA = 5, K_TRAP = 6, K_EV = 7 };
+/* NEXT-f2 (R50): migration / redirection messages travel in LSPD mode under
+ * the kind code of PROBE (unused there), the message in payload bits 28-30
+ * and a tag or node id in bits 0-27 */
+#define K_CTL K_PROBE
+enum { SUB_MR = 1, SUB_MG = 2, SUB_MN = 3, SUB_MIG = 4, SUB_DU = 5, SUB_INV = 6, SUB_RR = 7 };
+#define CTL(sub, v) (((uint32_t)(sub) << 28) | (v))
 /* core modes ("miss under a miss is not allowed"; DESIGN 3.4) */
 enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4, M_L1WAIT = 5 };
 
@@ -43,9 +49,25 @@ typedef struct {
 
 typedef struct { uint32_t kind, dst, payload, nfl; } Packet;   /* ToBeSend entry */
 
-typedef struct { int valid; uint32_t tag; uint64_t stamp; } Line;  /* L2 line */
+/* L2 line: tag, LRU stamp and, with migration (NEXT-f2, R44-R52),
+ * the "statistics counter" of the last N accessors as a ring,
+ * the migration state and its target: MIGREQ = migration requested from the
+ * directory, MIGSENT = block sent to mtarget, the source still serving
+ * (P:L78), FWD = an invalid "forwarding ghost" that remembers where the
+ * block went */
+enum { MS_NORMAL = 0, MS_MIGREQ = 1, MS_MIGSENT = 2, MS_FWD = 3 };
+#define MIG_HIST_MAX 16
+typedef struct {
+    int valid; uint32_t tag; uint64_t stamp;
+    int mstate; uint32_t mtarget;
+    uint32_t hist[MIG_HIST_MAX]; uint32_t hcount, hhead;
+} Line;
 
-typedef struct { uint32_t holder; uint32_t pend; } LocEntry;     /* location array */
+typedef struct {                                               /* location array */
+    uint32_t holder; uint32_t pend;
+    int transit;      /* NEXT-f2: a granted migration of T is in flight (R47)  */
+    int early_ev;     /* ... and its target already evicted T (R47)          */
+} LocEntry;
 
 /* private L1 line (NEXT-f1, R42): the block tag, last touch, and the node
  * whose L2 slice supplied it (where the victim writeback goes) */
@@ -68,6 +90,7 @@ typedef struct {
     L1Line *l1;        /* Core.L1 (NEXT-f1), l1_sets x l1_ways                 */
     uint64_t script_pos, script_end;
     uint64_t script_used;
+    struct { uint32_t tag, count; int used; } migrx[4];   /* inbound B2 reassembly (R52) */
 } Node;
 
 struct orc_sim {
@@ -209,17 +232,40 @@ static void enq(orc_sim *s, uint32_t n, uint32_t kind, uint32_t dst, uint32_t pa
  * L2 slice: set-associative, LRU with invalid-first and lowest-way ties
  * ("local victim selection"; R23, R24)
  * ---------------------------------------------------------------------- */
-static int l2_hit(orc_sim *s, uint32_t n, uint32_t T)
+/* the valid line holding T in n's slice, or NULL */
+static Line *l2_find(orc_sim *s, uint32_t n, uint32_t T)
 {
     uint32_t set = T % s->cfg.l2_sets;
     Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways];
-    for (uint32_t w = 0; w < s->cfg.l2_ways; ++w) {
-        if (L[w].valid && L[w].tag == T) {
-            L[w].stamp = s->t;
-            return 1;
-        }
+    for (uint32_t w = 0; w < s->cfg.l2_ways; ++w)
+        if (L[w].valid && L[w].tag == T) return &L[w];
+    return NULL;
+}
+
+/* NEXT-f2 "statistics counter ... last N accesses" (R45): a ring
+ * of the last mig_hist accessor ids, oldest dropped */
+static void record_access(orc_sim *s, Line *L, uint32_t who)
+{
+    uint32_t N = s->cfg.mig_hist;
+    if (!N) return;
+    if (L->hcount < N) {
+        L->hist[(L->hhead + L->hcount) % N] = who;
+        L->hcount += 1;
+    } else {
+        L->hist[L->hhead] = who;
+        L->hhead = (L->hhead + 1) % N;
     }
-    return 0;
+}
+
+/* L2HIT by accessor `who` (the owner for a local access, the requester for a
+ * served RQ): stamp update (R23) and, with migration, the access record */
+static int l2_hit(orc_sim *s, uint32_t n, uint32_t T, uint32_t who)
+{
+    Line *L = l2_find(s, n, T);
+    if (!L) return 0;
+    L->stamp = s->t;
+    record_access(s, L, who);
+    return 1;
 }
 
 /* Home node of tag T: the distributed directory (R12, T mod N) or, in the
@@ -235,6 +281,17 @@ static void ev_handler(orc_sim *s, uint32_t h, uint32_t T, uint32_t src)
 {
     (void)h;
     LocEntry *e = &s->loc[T];
+    if (e->transit) {
+        if (e->holder != src) {
+            /* NEXT-f2 (R47): the migration target evicted T before its
+             * directory update arrived; the update leaves the entry empty */
+            if (e->early_ev) fail(s, ORC_EASSERT, "two early EVs during one migration");
+            e->early_ev = 1;
+            s->c.evs_received += 1;
+            return;
+        }
+        e->transit = 0;   /* the source evicted T before sending it: migration aborted (R47) */
+    }
     if (e->holder != src) fail(s, ORC_EASSERT, "EV from a node that is not the recorded holder");
     if (e->pend > 0) e->pend -= 1;
     else e->holder = HOLDER_NONE;
@@ -250,8 +307,11 @@ static void install(orc_sim *s, uint32_t n, uint32_t T)
     Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways];
     uint32_t w, victim = 0;
     int found_invalid = 0;
+    /* NEXT-f2: a forwarding ghost of T itself is dropped (T lives here again) */
+    for (w = 0; w < s->cfg.l2_ways; ++w)
+        if (!L[w].valid && L[w].mstate == MS_FWD && L[w].tag == T) { L[w].mstate = MS_NORMAL; L[w].tag = 0; L[w].mtarget = 0; }
     for (w = 0; w < s->cfg.l2_ways; ++w) {
-        if (!L[w].valid) { victim = w; found_invalid = 1; break; }
+        if (!L[w].valid) { victim = w; found_invalid = 1; break; }   /* invalid (or a ghost) first */
     }
     if (!found_invalid) {
         victim = 0;
@@ -262,13 +322,25 @@ static void install(orc_sim *s, uint32_t n, uint32_t T)
         uint32_t V = L[victim].tag;
         uint32_t hv = home_of(s, V);
         s->c.evictions += 1;
-        s->c.evs_sent += 1;
-        if (hv == n) ev_handler(s, n, V, n);
-        else enq(s, n, K_EV, hv, V, 1);
+        if (L[victim].mstate == MS_MIGSENT) {
+            /* NEXT-f2 (R49): V is already on its way to the migration target,
+             * whose directory update takes the entry over: no EV */
+        } else {
+            s->c.evs_sent += 1;
+            if (hv == n) ev_handler(s, n, V, n);
+            else enq(s, n, K_EV, hv, V, 1);
+        }
     }
     L[victim].valid = 1;
     L[victim].tag = T;
     L[victim].stamp = s->t;
+    L[victim].mstate = MS_NORMAL;          /* a fresh residency: its history holds the
+                                              installing node's own access (R45) */
+    L[victim].mtarget = 0;
+    L[victim].hcount = 0;
+    L[victim].hhead = 0;
+    memset(L[victim].hist, 0, sizeof L[victim].hist);
+    record_access(s, &L[victim], n);
     s->c.installs += 1;
 }
 
@@ -325,13 +397,15 @@ static void complete(orc_sim *s, uint32_t n)
 
 /* Negative directory reply: fetch from memory, install at the requester
  * ("new request to next higher level memory"; P:L75 local placement). */
-static void receive_ndr(orc_sim *s, uint32_t n)
+#define NDR_NOINSTALL 0x80000000u   /* NEXT-f2 (R47): fetch without installing */
+#define NDR_PEND      0x40000000u   /* NEXT-f2 (R47): the reply counted an EV of the requester in flight */
+static void receive_ndr(orc_sim *s, uint32_t n, uint32_t payload)
 {
     Node *c = &s->nodes[n];
     if (c->mode != M_WAIT_DIR) fail(s, ORC_EASSERT, "NDR at a core that is not waiting for the directory");
     s->c.mem_requests += 1;
     c->mode = M_MEMWAIT;
-    c->install = 1;
+    c->install = (payload & NDR_NOINSTALL) ? 0 : (payload & NDR_PEND) ? 2 : 1;
     c->ready = s->t + s->cfg.mem_lat;
 }
 
@@ -354,18 +428,204 @@ static void dir_service(orc_sim *s, uint32_t h, uint32_t T, uint32_t r)
     if (e->holder == HOLDER_NONE) {
         e->holder = r;                     /* reserve: local placement */
         kind = K_NDR; payload = T;
+    } else if (e->holder == r && e->transit) {
+        /* NEXT-f2 (R47): r sent T away and dropped its copy; the block is on
+         * its way to the target: r fetches from memory without installing */
+        kind = K_NDR; payload = T | NDR_NOINSTALL;
     } else if (e->holder == r) {
         e->pend += 1;                      /* r's EV of T is still in flight (R13) */
         if (e->pend > PEND_MAX) fail(s, ORC_EOVERFLOW, "directory pend count overflow");
-        kind = K_NDR; payload = T;
+        kind = K_NDR; payload = T | (s->cfg.mig_hist ? NDR_PEND : 0u);
     } else {
         kind = K_DR; payload = e->holder;
     }
     if (r == h) {                          /* loopback: no flits (R28) */
-        if (kind == K_NDR) receive_ndr(s, r);
+        if (kind == K_NDR) receive_ndr(s, r, payload);
         else receive_dr(s, r, payload);
     } else {
         enq(s, h, kind, r, payload, 1);
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-f2: migration and redirection (Table I; SPEC
+ * S:L226-243; readings R44-R52 of DESIGN.md).
+ * ---------------------------------------------------------------------- */
+static void ctl_deliver(orc_sim *s, uint32_t at, uint32_t sub, uint32_t v, uint32_t src);
+static void serve_rq(orc_sim *s, uint32_t n, uint32_t T, uint32_t r);
+
+/* a 1-flit control message (sub, v) from `from` to `to`, or handled inline
+ * when to == from (no flits, R51) */
+static void ctl_send(orc_sim *s, uint32_t from, uint32_t to, uint32_t sub, uint32_t v)
+{
+    if (to == from) ctl_deliver(s, to, sub, v, from);
+    else enq(s, from, K_CTL, to, CTL(sub, v), 1);
+}
+
+/* "If a remote node have accessed it mostly, then migration get triggered.
+ * If a local node have accessed it most time than there is no need of
+ * migration" (SPEC should_migrate S:L235-243; R46): the node with the
+ * most history entries (ties: lowest id), if it is not the holder h and is
+ * strictly ahead of h; else none */
+static uint32_t mig_target(const orc_sim *s, const Line *L, uint32_t h)
+{
+    uint32_t N = s->cfg.mig_hist, best = HOLDER_NONE, bestc = 0, hc = 0;
+    for (uint32_t i = 0; i < L->hcount; ++i) {
+        uint32_t a = L->hist[(L->hhead + i) % N], cnt = 0;
+        for (uint32_t j = 0; j < L->hcount; ++j) cnt += L->hist[(L->hhead + j) % N] == a;
+        if (a == h) hc = cnt;
+        if (cnt > bestc || (cnt == bestc && a < best)) { best = a; bestc = cnt; }
+    }
+    return (best != HOLDER_NONE && best != h && bestc > hc) ? best : HOLDER_NONE;
+}
+
+/* "The check for a local cache migration may get triggered when a request
+ * comes from remote nodes": after an RQ served at h (R46, R47) */
+static void maybe_migrate(orc_sim *s, uint32_t h, Line *L)
+{
+    if (!s->cfg.mig_hist || L->mstate != MS_NORMAL) return;
+    uint32_t R = mig_target(s, L, h);
+    if (R == HOLDER_NONE) return;
+    L->mstate = MS_MIGREQ;
+    L->mtarget = R;
+    s->c.mig_requests += 1;
+    ctl_send(s, h, home_of(s, L->tag), SUB_MR, L->tag);
+}
+
+/* "whole cache block will be sent/migrate to that remote node":
+ * the B2 packet of nfl_b2 flits (Table I: 16), enqueued as <= 8-flit parts */
+static void send_block(orc_sim *s, uint32_t h, uint32_t R, uint32_t T)
+{
+    uint32_t left = s->cfg.nfl_b2;
+    while (left) {
+        uint32_t k = left > 8 ? 8 : left;
+        enq(s, h, K_CTL, R, CTL(SUB_MIG, T), k);
+        left -= k;
+    }
+}
+
+static void ctl_deliver(orc_sim *s, uint32_t at, uint32_t sub, uint32_t v, uint32_t src)
+{
+    switch (sub) {
+    case SUB_MR: {   /* at home(T): grant iff src holds T, no EV of T pending, none in flight */
+        LocEntry *e = &s->loc[v];
+        int ok = e->holder == src && e->pend == 0 && !e->transit;
+        if (ok) { e->transit = 1; e->early_ev = 0; }
+        ctl_send(s, at, src, ok ? SUB_MG : SUB_MN, v);
+        break;
+    }
+    case SUB_MG: {   /* at the holder: the block goes to the target (if still here) */
+        Line *L = l2_find(s, at, v);
+        if (!L || L->mstate != MS_MIGREQ) break;   /* evicted meanwhile: its EV aborts the transit (R47) */
+        L->mstate = MS_MIGSENT;
+        s->c.migrations += 1;
+        send_block(s, at, L->mtarget, v);
+        break;
+    }
+    case SUB_MN: {   /* refused: the line stays */
+        Line *L = l2_find(s, at, v);
+        s->c.mig_nacks += 1;
+        if (!L || L->mstate != MS_MIGREQ) break;
+        L->mstate = MS_NORMAL;
+        L->mtarget = 0;
+        break;
+    }
+    case SUB_MIG: {  /* a flit of an inbound block; the last one installs it */
+        Node *c = &s->nodes[at];
+        int k = -1;
+        for (int i = 0; i < 4; ++i) if (c->migrx[i].used && c->migrx[i].tag == v) k = i;
+        if (k < 0)
+            for (int i = 0; i < 4 && k < 0; ++i) if (!c->migrx[i].used) k = i;
+        if (k < 0) { fail(s, ORC_EOVERFLOW, "more than 4 inbound migrations at one node (R52)"); break; }
+        if (!c->migrx[k].used) { c->migrx[k].used = 1; c->migrx[k].tag = v; c->migrx[k].count = 0; }
+        c->migrx[k].count += 1;
+        if (c->migrx[k].count < s->cfg.nfl_b2) break;
+        c->migrx[k].used = 0; c->migrx[k].tag = 0; c->migrx[k].count = 0;
+        if (l2_find(s, at, v)) { fail(s, ORC_EASSERT, "migrated block already present at the target"); break; }
+        install(s, at, v);
+        s->c.mig_installs += 1;
+        ctl_send(s, at, home_of(s, v), SUB_DU, v);   /* "directory get updated" */
+        break;
+    }
+    case SUB_DU: {   /* at home(T): the target holds T now; the source invalidates */
+        LocEntry *e = &s->loc[v];
+        if (!e->transit) { fail(s, ORC_EASSERT, "directory update without a migration in flight"); break; }
+        uint32_t h = e->holder;
+        e->transit = 0;
+        s->c.dir_updates += 1;
+        if (e->early_ev) { e->early_ev = 0; e->holder = HOLDER_NONE; }
+        else e->holder = src;
+        ctl_send(s, at, h, SUB_INV, v);
+        break;
+    }
+    case SUB_INV: {  /* "source packet invalidates its copy": a forwarding ghost stays */
+        Line *L = l2_find(s, at, v);
+        s->c.invalidations += 1;
+        if (!L || L->mstate != MS_MIGSENT) break;   /* already replaced (R49) */
+        L->valid = 0;
+        L->mstate = MS_FWD;                    /* tag and mtarget kept (R48) */
+        L->stamp = 0;
+        L->hcount = 0; L->hhead = 0;
+        memset(L->hist, 0, sizeof L->hist);
+        break;
+    }
+    case SUB_RR: {   /* "Reply redirection" (Table I; R48): ask the new holder v */
+        Node *c = &s->nodes[at];
+        if (c->mode != M_WAIT_DATA) { fail(s, ORC_EASSERT, "redirection at a core not waiting for data"); break; }
+        s->c.rr_received += 1;
+        s->c.requests_made += 1;
+        if (v == at) serve_rq(s, at, c->tag, at);   /* the block came to the requester itself */
+        else enq(s, at, K_RQ, v, c->tag, 1);
+        break;
+    }
+    default:
+        fail(s, ORC_EASSERT, "unknown control message");
+    }
+}
+
+/* RQ for T from requester r at node n (Fig. 4 step 4): serve from the
+ * slice (RA, nfl_ra flits), else redirect through a forwarding ghost
+ * (NEXT-f2), else TRAP.  r == n only for a redirection to the
+ * requester itself, served inline (R51). */
+static void serve_rq(orc_sim *s, uint32_t n, uint32_t T, uint32_t r)
+{
+    s->c.requests_received += 1;
+    Line *L = l2_find(s, n, T);
+    if (L) {
+        L->stamp = s->t;
+        record_access(s, L, r);
+        s->c.replies_sent += 1;
+        if (r == n) {
+            s->c.replies_received += 1;
+            l1_fill(s, n, T, n);
+            complete(s, n);
+        } else {
+            enq(s, n, K_RA, r, T, s->cfg.nfl_ra);
+        }
+        maybe_migrate(s, n, L);
+        return;
+    }
+    if (s->cfg.mig_hist && r != n) {
+        uint32_t set = T % s->cfg.l2_sets;
+        Line *G = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways];
+        for (uint32_t w = 0; w < s->cfg.l2_ways; ++w) {
+            if (!G[w].valid && G[w].mstate == MS_FWD && G[w].tag == T) {
+                s->c.redirections += 1;
+                ctl_send(s, n, r, SUB_RR, G[w].mtarget);
+                return;
+            }
+        }
+    }
+    s->c.traps_sent += 1;                         /* "send the invalid packet" */
+    if (r == n) {
+        Node *c = &s->nodes[n];
+        s->c.traps_received += 1;
+        s->c.mem_requests += 1;
+        c->mode = M_MEMWAIT;
+        c->install = 0;
+        c->ready = s->t + s->cfg.mem_lat;
+    } else {
+        enq(s, n, K_TRAP, r, T, 1);
     }
 }
 
@@ -373,7 +633,7 @@ static void dir_service(orc_sim *s, uint32_t h, uint32_t T, uint32_t r)
 static void l2_access(orc_sim *s, uint32_t n, uint32_t T)
 {
     Node *c = &s->nodes[n];
-    if (l2_hit(s, n, T)) {
+    if (l2_hit(s, n, T, n)) {
         s->c.l2_hits += 1;
         if (s->cfg.l2_hit_lat == 0) {
             l1_fill(s, n, T, n);
@@ -484,7 +744,19 @@ static void phase1(orc_sim *s, uint32_t n)
         complete(s, n);
     }
     if (c->mode == M_MEMWAIT && c->ready == s->t) {
-        if (c->install) install(s, n, c->tag);
+        if (c->install && s->cfg.mig_hist && l2_find(s, n, c->tag)) {
+            /* NEXT-f2 (R47): the block migrated here while this fetch was in
+             * flight: no second copy; if the directory counted an EV of ours
+             * that does not exist, one is sent to even it */
+            if (c->install == 2) {
+                uint32_t hv = home_of(s, c->tag);
+                s->c.evs_sent += 1;
+                if (hv == n) ev_handler(s, n, c->tag, n);
+                else enq(s, n, K_EV, hv, c->tag, 1);
+            }
+        } else if (c->install) {
+            install(s, n, c->tag);
+        }
         l1_fill(s, n, c->tag, n);                 /* R42: a memory fill is supplied locally */
         complete(s, n);
     }
@@ -706,8 +978,9 @@ static void phase3(orc_sim *s, uint32_t n)
     hist_add(s, s->hl, s->t - f.inj);
     hist_add(s, s->hd, f.age);
     switch (f.kind) {
-    case K_PROBE:
-        s->c.probes_delivered += 1;
+    case K_PROBE:                                 /* = K_CTL in LSPD mode (R50) */
+        if (s->cfg.mode == ORC_MODE_LSPD) ctl_deliver(s, n, f.payload >> 28, f.payload & 0x0FFFFFFFu, f.src);
+        else s->c.probes_delivered += 1;
         break;
     case K_DA:
         dir_service(s, n, f.payload, f.src);
@@ -716,17 +989,10 @@ static void phase3(orc_sim *s, uint32_t n)
         receive_dr(s, n, f.payload);
         break;
     case K_NDR:
-        receive_ndr(s, n);
+        receive_ndr(s, n, f.payload);
         break;
     case K_RQ:
-        s->c.requests_received += 1;
-        if (l2_hit(s, n, f.payload)) {
-            s->c.replies_sent += 1;
-            enq(s, n, K_RA, f.src, f.payload, s->cfg.nfl_ra);
-        } else {
-            s->c.traps_sent += 1;                 /* "send the invalid packet" */
-            enq(s, n, K_TRAP, f.src, f.payload, 1);
-        }
+        serve_rq(s, n, f.payload, f.src);
         break;
     case K_RA:
         if (c->mode != M_WAIT_DATA) fail(s, ORC_EASSERT, "RA flit at a core not waiting for data");
@@ -781,7 +1047,7 @@ static void check_invariants(orc_sim *s)
         for (uint32_t n = 0; n < s->N; ++n)
             for (uint32_t i = 0; i < lines; ++i) {
                 Line *L = &s->nodes[n].l2[i];
-                if (!L->valid) continue;
+                if (!L->valid || L->mstate == MS_MIGSENT) continue;   /* + one source copy in transit (R47) */
                 if (seen[L->tag]) fail(s, ORC_EASSERT, "block valid in two slices");
                 seen[L->tag] = 1;
             }
@@ -853,6 +1119,12 @@ int orc_create(const orc_config *cfg, orc_sim **out)
     }
     if (cfg->hist_bins == 0 || cfg->hist_bins > 65536) { set_err("hist_bins must be 1..65536"); return ORC_EINVAL; }
     if (cfg->age_base > AGE_MAX) { set_err("age_base > 65535 (R32)"); return ORC_EINVAL; }
+    if (cfg->mig_hist > MIG_HIST_MAX) { set_err("mig_hist must be 0..16"); return ORC_EINVAL; }
+    if (cfg->mig_hist && (cfg->mode != ORC_MODE_LSPD || cfg->nfl_b2 < 1 || cfg->nfl_b2 > 16 ||
+                          (uint64_t)cfg->tags_per_node * cfg->mesh_w * cfg->mesh_h > (1ull << 28))) {
+        set_err("migration needs LSPD mode, nfl_b2 1..16 and a tag space <= 2^28 (R50)");
+        return ORC_EINVAL;
+    }
     if (cfg->nfl_ra < 1 || cfg->nfl_ra > 8) { set_err("nfl_ra must be 1..8"); return ORC_EINVAL; }
     uint64_t N = (uint64_t)W * H;
     if (cfg->mode == ORC_MODE_LSPD) {
@@ -898,7 +1170,9 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         s->l1_store = calloc(N * l1lines + 1, sizeof(L1Line));
         bad = !s->l2_store || !s->loc || !s->l1_store;
         if (!bad) {
-            for (uint64_t T = 0; T < s->ntags; ++T) { s->loc[T].holder = HOLDER_NONE; s->loc[T].pend = 0; }
+            for (uint64_t T = 0; T < s->ntags; ++T) {
+                s->loc[T].holder = HOLDER_NONE; s->loc[T].pend = 0; s->loc[T].transit = 0; s->loc[T].early_ev = 0;
+            }
             for (uint64_t n = 0; n < N; ++n) {
                 s->nodes[n].l2 = &s->l2_store[n * lines];
                 s->nodes[n].l1 = &s->l1_store[n * l1lines];
@@ -1016,7 +1290,8 @@ static uint64_t term(uint64_t dom, uint64_t idx, const uint64_t *v, int k)
 }
 
 enum { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, D_LOC = 6,
-       D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10, D_L1 = 11 };
+       D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10, D_L1 = 11, D_L2MIG = 12, D_LOCMIG = 13,
+       D_MIGRX = 14 };
 
 uint64_t orc_state_hash(const orc_sim *s)
 {
@@ -1069,9 +1344,32 @@ uint64_t orc_state_hash(const orc_sim *s)
                 }
         }
         if (c->script_used) { v[0] = c->script_used; H += term(D_SCRIPT, n, v, 1); }
+        if (s->cfg.mode == ORC_MODE_LSPD && s->cfg.mig_hist) {
+            /* NEXT-f2: per line (state, target, history oldest first) when any is set */
+            uint32_t S = s->cfg.l2_sets, Wy = s->cfg.l2_ways;
+            for (uint32_t st = 0; st < S; ++st)
+                for (uint32_t w = 0; w < Wy; ++w) {
+                    const Line *L = &c->l2[(uint64_t)st * Wy + w];
+                    if (L->mstate == MS_NORMAL && (!L->valid || L->hcount == 0)) continue;
+                    uint64_t u[4 + MIG_HIST_MAX];
+                    int k = 0;
+                    u[k++] = (uint64_t)L->mstate; u[k++] = L->tag; u[k++] = L->mtarget; u[k++] = L->hcount;
+                    for (uint32_t i = 0; i < L->hcount; ++i) u[k++] = L->hist[(L->hhead + i) % s->cfg.mig_hist];
+                    H += mix64(mix64(((uint64_t)D_L2MIG << 56) ^ (((uint64_t)n * S + st) * Wy + w)) ^ tuple_hash(u, k));
+                }
+            for (int i = 0; i < 4; ++i)
+                if (c->migrx[i].used) {
+                    v[0] = c->migrx[i].tag; v[1] = c->migrx[i].count;
+                    H += term(D_MIGRX, ((uint64_t)n << 2) + (uint64_t)i, v, 2);
+                }
+        }
     }
     for (uint64_t T = 0; T < s->ntags; ++T) {
         const LocEntry *e = &s->loc[T];
+        if (e->transit || e->early_ev) {
+            v[0] = (uint64_t)e->transit; v[1] = (uint64_t)e->early_ev;
+            H += term(D_LOCMIG, T, v, 2);
+        }
         if (e->holder == HOLDER_NONE && e->pend == 0) continue;
         v[0] = e->holder == HOLDER_NONE ? 0 : (uint64_t)e->holder + 1;
         v[1] = e->pend;
@@ -1136,7 +1434,7 @@ int orc_check_directory_quiescent(const orc_sim *s)
             holder[L->tag] = n;
         }
     for (uint64_t T = 0; T < s->ntags && !bad; ++T) {
-        if (s->loc[T].holder != holder[T] || s->loc[T].pend != 0) bad = 1;
+        if (s->loc[T].holder != holder[T] || s->loc[T].pend != 0 || s->loc[T].transit || s->loc[T].early_ev) bad = 1;
     }
     free(holder);
     return bad ? -1 : 0;
@@ -1260,4 +1558,54 @@ int orc_poke(orc_sim *s, uint32_t field, uint32_t n, uint32_t i, uint32_t j, uin
     case 13: if (!c) return ORC_EINVAL; c->ready += value; return ORC_OK;
     }
     return ORC_EINVAL;
+}
+
+/* NEXT-f2 test hook: the migration decision of R46 on a given accessor history
+ * (oldest first) for holder h: the target node, or UINT32_MAX for none. */
+uint32_t orc_mig_target(const uint32_t *hist, uint32_t count, uint32_t holder)
+{
+    Line L;
+    memset(&L, 0, sizeof L);
+    orc_sim tmp;
+    memset(&tmp, 0, sizeof tmp);
+    tmp.cfg.mig_hist = count ? count : 1;
+    for (uint32_t i = 0; i < count && i < MIG_HIST_MAX; ++i) L.hist[i] = hist[i];
+    L.hcount = count < MIG_HIST_MAX ? count : MIG_HIST_MAX;
+    return mig_target(&tmp, &L, holder);
+}
+
+/* NEXT-f2 peek: L2 line (n, set, way) migration state: mstate, mtarget, hcount;
+ * loc entry T: transit, early_ev. */
+int orc_l2_mig(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint64_t out[3])
+{
+    if (s->cfg.mode != ORC_MODE_LSPD || n >= s->N || set >= s->cfg.l2_sets || way >= s->cfg.l2_ways)
+        return ORC_EINVAL;
+    const Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways + way];
+    out[0] = (uint64_t)L->mstate; out[1] = L->mtarget; out[2] = L->hcount;
+    return ORC_OK;
+}
+
+int orc_loc_mig(const orc_sim *s, uint32_t T, uint64_t out[2])
+{
+    if (T >= s->ntags) return ORC_EINVAL;
+    out[0] = (uint64_t)s->loc[T].transit; out[1] = (uint64_t)s->loc[T].early_ev;
+    return ORC_OK;
+}
+
+/* NEXT-f2 peeks: the accessor history of L2 line (n, set, way), oldest first
+ * (returns the count); inbound-migration slot k of node n: used, tag, count */
+int orc_l2_hist(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint32_t out[16])
+{
+    if (s->cfg.mode != ORC_MODE_LSPD || n >= s->N || set >= s->cfg.l2_sets || way >= s->cfg.l2_ways)
+        return -1;
+    const Line *L = &s->nodes[n].l2[(uint64_t)set * s->cfg.l2_ways + way];
+    for (uint32_t i = 0; i < L->hcount; ++i) out[i] = L->hist[(L->hhead + i) % (s->cfg.mig_hist ? s->cfg.mig_hist : 1)];
+    return (int)L->hcount;
+}
+
+int orc_migrx(const orc_sim *s, uint32_t n, uint32_t k, uint64_t out[3])
+{
+    if (n >= s->N || k >= 4) return ORC_EINVAL;
+    out[0] = (uint64_t)s->nodes[n].migrx[k].used; out[1] = s->nodes[n].migrx[k].tag; out[2] = s->nodes[n].migrx[k].count;
+    return ORC_OK;
 }

@@ -70,6 +70,8 @@ typedef struct {
     uint32_t l1_miss_lat;        /* "L1 miss cycle" countdown, >= 1 */
     uint32_t inject_mode;        /* 0: R7; 1: an ejecting flit frees its slot (NEXT-f4) */
     uint32_t age_base;           /* test knob: age of a newly injected flit (0 = P:L259) */
+    uint32_t mig_hist;           /* NEXT-f2: accessor history length N; 0 = no migration */
+    uint32_t nfl_b2;             /* NEXT-f2: flits of a B2 block migration (Table I: 16), 1..16 */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */
@@ -82,6 +84,8 @@ typedef struct {
     int64_t installs, evictions, evs_sent, evs_received;
     int64_t drops[8];
     int64_t l1_hits, l1_misses, wb_sent, wb_received;   /* NEXT-f1 (R42) */
+    int64_t mig_requests, mig_nacks, migrations, mig_installs;   /* NEXT-f2 (R44-R52) */
+    int64_t dir_updates, invalidations, redirections, rr_received;
 } orc_counters;
 
 typedef struct orc_sim orc_sim;
@@ -135,6 +139,14 @@ int  orc_l1_line(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint6
 int64_t orc_script_used(const orc_sim *s, uint32_t n);
 /* The simulation's generator call for (n, t): out = {fired, UR dst or LSPD tag}. */
 int  orc_gen(const orc_sim *s, uint32_t n, uint64_t t, uint64_t out[2]);
+/* NEXT-f2: the migration decision (R46) on an accessor history, oldest first:
+ * the target node, or UINT32_MAX for none (SPEC S:L235-243 examples). */
+uint32_t orc_mig_target(const uint32_t *hist, uint32_t count, uint32_t holder);
+/* NEXT-f2 peeks: L2 line migration state {mstate, mtarget, hcount}; loc {transit, early_ev}. */
+int  orc_l2_mig(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint64_t out[3]);
+int  orc_loc_mig(const orc_sim *s, uint32_t T, uint64_t out[2]);
+int  orc_l2_hist(const orc_sim *s, uint32_t n, uint32_t set, uint32_t way, uint32_t out[16]);
+int  orc_migrx(const orc_sim *s, uint32_t n, uint32_t k, uint64_t out[3]);
 /* Test-only single-field mutation (hash sensitivity pins); fields in noc_oracle.c. */
 int  orc_poke(orc_sim *s, uint32_t field, uint32_t n, uint32_t i, uint32_t j, uint64_t value);
 

@@ -32,6 +32,7 @@ BASE = dict(
     l2_hit_lat=1, mem_lat=100, nfl_ra=4,
     sendq_cap=16, hist_bins=4096, seed=1, route=0, dir_mode=0, dir_node=0,
     l1_sets=0, l1_ways=2, l1_miss_lat=2, inject_mode=0, age_base=0, band_streams=0,
+    mig_hist=0, nfl_b2=16,
 )
 
 

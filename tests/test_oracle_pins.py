@@ -45,7 +45,7 @@ def term(dom, idx, vals):
     return mix(mix(((dom << 56) ^ idx) & M64) ^ tup(vals))
 
 
-LINK, FIFO, FIFONEXT, CORE, L2, LOC, CNT, HIST, CYCLE, SCRIPT, L1 = range(1, 12)
+LINK, FIFO, FIFONEXT, CORE, L2, LOC, CNT, HIST, CYCLE, SCRIPT, L1, L2MIG, LOCMIG, MIGRX = range(1, 15)
 IDLE, L2WAIT, WAIT_DIR, WAIT_DATA, MEMWAIT, L1WAIT = range(6)
 
 
@@ -53,7 +53,9 @@ def snapshot(o, cfg):
     """The raw state, field by field, through the oracle's peeks."""
     N = cfg["mesh_w"] * cfg["mesh_h"]
     lspd = cfg["mode"] == W.MODE_LSPD
-    st = {"links": {}, "fifo": {}, "core": {}, "l2": {}, "l1": {}, "loc": {}, "script": {}}
+    st = {"links": {}, "fifo": {}, "core": {}, "l2": {}, "l1": {}, "loc": {}, "script": {},
+          "l2mig": {}, "locmig": {}, "migrx": {}}
+    mig = lspd and cfg.get("mig_hist", 0) > 0
     for n in range(N):
         for d in range(4):
             f = o.link(n, d)
@@ -62,10 +64,15 @@ def snapshot(o, cfg):
         st["fifo"][n] = o.fifo(n)
         st["core"][n] = o.core(n)
         st["script"][n] = o.script_used(n)
+        if mig:
+            for k in range(4):
+                st["migrx"][(n, k)] = o.migrx(n, k)
         if lspd:
             for s in range(cfg["l2_sets"]):
                 for w in range(cfg["l2_ways"]):
                     st["l2"][(n, s, w)] = o.l2_line(n, s, w)
+                    if mig:
+                        st["l2mig"][(n, s, w)] = o.l2_mig(n, s, w) + (o.l2_hist(n, s, w),)
             if cfg["l1_sets"]:
                 for s in range(cfg["l1_sets"]):
                     for w in range(cfg["l1_ways"]):
@@ -73,6 +80,8 @@ def snapshot(o, cfg):
     if lspd:
         for T in range(cfg["tags_per_node"] * N):
             st["loc"][T] = o.loc(T)
+            if mig:
+                st["locmig"][T] = o.loc_mig(T)
     cnt, hl, hd, ha = o.stats()
     st["cnt"], st["hist"], st["cycle"] = cnt, (hl, hd, ha), cnt["cycle"]
     return st
@@ -119,6 +128,19 @@ def design_hash(st, cfg):
             if v:
                 terms.append(add(HIST, (h << 32) + b, [v]))
     terms.append(add(CYCLE, 0, [st["cycle"]]))
+    # NEXT-f2 (DESIGN 3.7 domains 12-14): line migration state and history,
+    # directory transit flags, inbound migration reassembly slots
+    for (n, s_, w), (mstate, mtarget, hcount, hist) in st["l2mig"].items():
+        valid, tag = st["l2"][(n, s_, w)][:2]
+        if mstate == 0 and (not valid or hcount == 0):
+            continue
+        terms.append(add(L2MIG, (n * S + s_) * Wy + w, [mstate, tag, mtarget, hcount] + list(hist)))
+    for T, (transit, early) in st["locmig"].items():
+        if transit or early:
+            terms.append(add(LOCMIG, T, [transit, early]))
+    for (n, k), (used, tag, count) in st["migrx"].items():
+        if used:
+            terms.append(add(MIGRX, (n << 2) + k, [tag, count]))
     for n, used in st["script"].items():
         if used:
             terms.append(add(SCRIPT, n, [used]))
@@ -127,20 +149,23 @@ def design_hash(st, cfg):
     return H
 
 
-# counters in the order of DESIGN 3.6 (hash index 0..34)
+# counters in the order of DESIGN 3.6 (hash index 0..42)
 W_COUNTERS = ("generated", "packets_enqueued", "injected", "ejected", "hops", "deflections",
               "probes_delivered", "accesses", "completed", "l2_hits", "l2_misses",
               "dir_searches", "requests_made", "requests_received", "replies_sent",
               "replies_received", "traps_sent", "traps_received", "mem_requests",
               "installs", "evictions", "evs_sent", "evs_received",
               "drops_probe", "drops_da", "drops_dr", "drops_ndr", "drops_rq", "drops_ra",
-              "drops_trap", "drops_ev", "l1_hits", "l1_misses", "wb_sent", "wb_received")
+              "drops_trap", "drops_ev", "l1_hits", "l1_misses", "wb_sent", "wb_received",
+              "mig_requests", "mig_nacks", "migrations", "mig_installs", "dir_updates", "invalidations",
+              "redirections", "rr_received")
 
 
 def _busy_lspd(w, h, **kw):
     kw.setdefault("lam", 0.3)
+    kw.setdefault("sendq_cap", 8)
     return W.make(mesh_w=w, mesh_h=h, mode=W.MODE_LSPD, l2_sets=2, l2_ways=2, tags_per_node=8,
-                  priv_tags=4, mem_lat=7, sendq_cap=8, hist_bins=64, **kw)
+                  priv_tags=4, mem_lat=7, hist_bins=64, **kw)
 
 
 HASH_CASES = {
@@ -151,6 +176,7 @@ HASH_CASES = {
     "lspd3x3": _busy_lspd(3, 3, seed=3),
     "lspd3x3_l1": _busy_lspd(3, 3, seed=5, l1_sets=1, l1_ways=2, l1_miss_lat=2),
     "lspd3x3_central": _busy_lspd(3, 3, seed=2, dir_mode=W.DIR_CENTRAL, dir_node=4),
+    "lspd3x3_mig": _busy_lspd(3, 3, seed=6, mig_hist=3, nfl_b2=5, sendq_cap=64),
 }
 
 
@@ -300,3 +326,20 @@ def test_generator_fire_rate_and_simulation_use_it():
                 assert f and tag == c["tag"]
                 checked += 1
     assert checked > 20
+
+
+def test_state_hash_definition_through_migrations():
+    """The NEXT-f2 domains (line migration state and history, directory
+    transit flags, inbound reassembly slots) at every third cycle of a run
+    with migrations in flight: DESIGN 3.7 equals the oracle's hash."""
+    cfg = HASH_CASES["lspd3x3_mig"]
+    o = Oracle(cfg)
+    seen = collections.Counter()
+    for _ in range(60):
+        o.run(3)
+        st = snapshot(o, cfg)
+        assert o.state_hash() == design_hash(st, cfg)
+        seen["line"] += sum(1 for v in st["l2mig"].values() if v[0] > 0)
+        seen["loc"] += sum(1 for v in st["locmig"].values() if v[0] or v[1])
+        seen["rx"] += sum(1 for v in st["migrx"].values() if v[0])
+    assert seen["line"] and seen["loc"] and seen["rx"] and o.stats()[0]["migrations"] > 0
