@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define NOC_SIM_ABI_VERSION 4u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base; 4: band_streams */
+#define NOC_SIM_ABI_VERSION 5u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base; 4: band_streams; 5: migration */
 
 /* error codes */
 #define NOC_OK          0
@@ -136,7 +136,13 @@ typedef struct noc_sim_config {
                                   cooperative launch, a barrier) and events
                                   in place of the NCCL barrier; 0 = all bands
                                   in one launch.  Results are identical     */
-    uint32_t reserved[2];      /* must be 0                                        */
+    uint32_t mig_hist;         /* LSPD, NEXT-f2 migration + redirection (DESIGN
+                                  R44-R52): length N of each L2 line's accessor
+                                  history ("last N (say 10) accesses"),
+                                  1..16; 0 = no migration (the base model).
+                                  Needs tags_per_node*N <= 2^28              */
+    uint32_t nfl_b2;           /* flits of a B2 block migration (Table I: 16),
+                                  1..16 (ignored when mig_hist = 0)          */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list
@@ -150,6 +156,11 @@ typedef struct noc_sim_counters {
     int64_t installs, evictions, evs_sent, evs_received;
     int64_t drops[8];          /* by kind: PROBE DA DR NDR RQ RA TRAP EV           */
     int64_t l1_hits, l1_misses, wb_sent, wb_received;   /* NEXT-f1 L1 (R42)       */
+    /* NEXT-f2 migration + redirection (R44-R52): requests to the directory,
+     * refusals, blocks sent, blocks installed at the target, directory
+     * updates, source invalidations, redirections sent / received */
+    int64_t mig_requests, mig_nacks, migrations, mig_installs;
+    int64_t dir_updates, invalidations, redirections, rr_received;
 } noc_sim_counters;
 
 /* Runtime facts about a handle (for measurement and the bench). */

@@ -22,10 +22,33 @@ enum : uint32_t {
     C_GENERATED = 0, C_ENQ, C_INJECTED, C_EJECTED, C_HOPS, C_DEFL, C_PROBES, C_ACCESSES,
     C_COMPLETED, C_L2HIT, C_L2MISS, C_DIRSEARCH, C_REQMADE, C_REQRCVD, C_REPSENT, C_REPRCVD,
     C_TRAPSENT, C_TRAPRCVD, C_MEMREQ, C_INSTALLS, C_EVICTIONS, C_EVSENT, C_EVRCVD,
-    C_DROPS = 23, C_L1HIT = 31, C_L1MISS, C_WBSENT, C_WBRCVD, NCOUNTERS = 35
+    C_DROPS = 23, C_L1HIT = 31, C_L1MISS, C_WBSENT, C_WBRCVD,
+    // NEXT-f2 migration + redirection (R44-R52)
+    C_MIGREQ = 35, C_MIGNACK, C_MIGS, C_MIGINST, C_DIRUPD, C_INVAL, C_REDIR, C_RRRCVD, NCOUNTERS = 43
 };
+// NEXT-f2 (R50): migration / redirection messages use the PROBE kind code in
+// LSPD mode, the message in payload bits 28-30, a tag or node id in bits 0-27
+enum : uint32_t { SUB_MR = 1, SUB_MG = 2, SUB_MN = 3, SUB_MIG = 4, SUB_DU = 5, SUB_INV = 6, SUB_RR = 7 };
+__host__ __device__ __forceinline__ uint32_t ctl_word(uint32_t sub, uint32_t v) { return (sub << 28) | v; }
+// NDR payload flags (NEXT-f2, R47): fetch without installing / the reply
+// counted an EV of the requester in flight
+constexpr uint32_t NDR_NOINSTALL = 0x80000000u, NDR_PEND = 0x40000000u;
+// L2 line word w (NEXT-f2): migration state [30:32) | history count [25:30) |
+// history head [21:25) | target node [0:21); state 0 NORMAL, 1 MIGREQ,
+// 2 MIGSENT, 3 FWD (an invalid forwarding ghost that keeps tag and target)
+enum : uint32_t { MS_NORMAL = 0, MS_MIGREQ = 1, MS_MIGSENT = 2, MS_FWD = 3 };
+__host__ __device__ __forceinline__ uint32_t lw_state(uint32_t w) { return w >> 30; }
+__host__ __device__ __forceinline__ uint32_t lw_count(uint32_t w) { return (w >> 25) & 31u; }
+__host__ __device__ __forceinline__ uint32_t lw_head(uint32_t w) { return (w >> 21) & 15u; }
+__host__ __device__ __forceinline__ uint32_t lw_target(uint32_t w) { return w & 0x1FFFFFu; }
+__host__ __device__ __forceinline__ uint32_t lw_make(uint32_t st, uint32_t cnt, uint32_t head, uint32_t tgt)
+{
+    return (st << 30) | (cnt << 25) | (head << 21) | tgt;
+}
+// a line holds a block iff tag+1 != 0 and it is not a forwarding ghost
+__host__ __device__ __forceinline__ bool line_valid(const uint4 &v) { return v.x != 0u && lw_state(v.w) != MS_FWD; }
 // error flags
-enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8, ERR_DROP = 16 };
+enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8, ERR_DROP = 16, ERR_MIGRX = 32 };
 
 constexpr uint32_t AGE_MAX = 65535u;   // R32
 constexpr uint32_t LIFE_MAX = (1u << 27) - 1u;   // R32: flit lifetime t - inj
@@ -135,7 +158,8 @@ __host__ __device__ __forceinline__ uint64_t hterm(uint64_t dom, uint64_t idx, u
 }
 
 enum : uint64_t { D_LINK = 1, D_FIFO = 2, D_FIFONEXT = 3, D_CORE = 4, D_L2 = 5, D_LOC = 6,
-                  D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10, D_L1 = 11 };
+                  D_CNT = 7, D_HIST = 8, D_CYCLE = 9, D_SCRIPT = 10, D_L1 = 11, D_L2MIG = 12, D_LOCMIG = 13,
+                  D_MIGRX = 14 };
 
 // ---------------------------------------------------------------------------
 // Device view of one simulation (passed by value to every kernel).
@@ -150,6 +174,7 @@ struct Dev {
     uint32_t l1_sets, l1_ways, l1_miss_lat;   // NEXT-f1 private L1 (R42); 0 sets = none
     uint32_t inject_mode;             // NEXT-f4: an ejecting flit frees its slot (R43)
     uint32_t age_base;                // test knob: age of an injected flit (0 = P:L259)
+    uint32_t mig_hist, nfl_b2;        // NEXT-f2: accessor history length (0 = off), B2 flits
     uint64_t loc_n;                   // directory entries held by this band
     uint32_t qcap, nb, seed_lo, seed_hi;
     uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi
@@ -165,6 +190,9 @@ struct Dev {
     uint4 *l2;                        // [nloc][sets][ways] {tag+1 (0 = invalid), stamp_lo, stamp_hi, 0}
     uint4 *l1;                        // [nloc][l1_sets][l1_ways] {tag+1, stamp_lo, stamp_hi, owner} (NEXT-f1)
     uint32_t *loc;                    // [tpn][nloc] directory entries of tags homed in this band
+    uint8_t *loc_mig;                 // NEXT-f2: per entry bit 0 migration in transit, bit 1 early EV
+    uint32_t *l2h;                    // NEXT-f2: [nloc][sets][ways][mig_hist] accessor ring
+    uint2 *migrx;                     // NEXT-f2: [nloc][4] inbound migrations {tag, flits} (flits 0 = free)
     const uint4 *script;              // [n_script] {cycle_lo, cycle_hi, value, 0} grouped by node
     const uint32_t *script_off;       // [nloc+1]
     uint32_t *script_pos;             // [nloc] events consumed

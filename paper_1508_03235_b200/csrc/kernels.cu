@@ -255,8 +255,8 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
                 case ML2WAIT: ready = r29; break;
                 case ML1WAIT: ready = r29; tag = cold.z; break;
                 case MWAITDIR: tag = cold.z; break;
-                case MWAITDATA: tag = cold.z; rx = cold.w >> 1; break;
-                default: ready = r29; tag = cold.z; inst = cold.w & 1u; break;
+                case MWAITDATA: tag = cold.z; rx = cold.w >> 2; break;
+                default: ready = r29; tag = cold.z; inst = cold.w & 3u; break;
                 }
                 TupleHash th(6);
                 th.add(mode).add(ready).add(tag).add(inst).add(start).add(rx);
@@ -265,10 +265,27 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
             const uint4 *L = S.l2 + (size_t)l * S.sets * S.ways;
             for (uint32_t i = 0; i < S.sets * S.ways; ++i) {
                 uint4 v = L[i];
-                if (v.x == 0u) continue;
+                if (S.mig_hist) {
+                    // NEXT-f2: (state, tag, target, history count, history oldest first)
+                    const uint32_t st = lw_state(v.w), cnt = lw_count(v.w);
+                    if (st != MS_NORMAL || (line_valid(v) && cnt)) {
+                        const size_t li = (size_t)l * S.sets * S.ways + i;
+                        const uint32_t N = S.mig_hist, head = lw_head(v.w);
+                        TupleHash th(4 + (int)cnt);
+                        th.add(st).add(v.x ? v.x - 1u : 0u).add(lw_target(v.w)).add(cnt);
+                        for (uint32_t k = 0; k < cnt; ++k) th.add(S.l2h[li * N + (head + k) % N]);
+                        H += hterm(D_L2MIG, (n * S.sets) * S.ways + i, th.h);
+                    }
+                }
+                if (!line_valid(v)) continue;
                 uint64_t stamp = ((uint64_t)v.z << 32) | v.y;
                 H += hterm(D_L2, (n * S.sets) * S.ways + i, TupleHash(2).add(v.x - 1u).add(stamp).h);
             }
+            if (S.mig_hist)
+                for (uint32_t k = 0; k < 4u; ++k) {
+                    const uint2 x = S.migrx[(size_t)l * 4u + k];
+                    if (x.y) H += hterm(D_MIGRX, (n << 2) + k, TupleHash(2).add(x.x).add(x.y).h);
+                }
             if (S.l1_sets) {   // NEXT-f1 L1 lines: (tag, stamp, owner)
                 const uint4 *M = S.l1 + (size_t)l * S.l1_sets * S.l1_ways;
                 for (uint32_t i = 0; i < S.l1_sets * S.l1_ways; ++i) {
@@ -304,13 +321,15 @@ __global__ void k_hash_loc(Dev S, unsigned long long *out)
     const uint64_t total = S.loc_n;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t e = S.loc[i];
-        if (!e) continue;
+        const uint32_t m = S.mig_hist ? S.loc_mig[i] : 0u;
+        if (!e && !m) continue;
         uint64_t T = i;   // centralized: the entry index is the tag
         if (!S.dir_mode) {
             const uint64_t q = i / S.nloc, lh = i - q * S.nloc;
             T = q * S.N + S.n0 + lh;
         }
-        H += hterm(D_LOC, T, TupleHash(2).add(e & HOLDER_MASK).add(e >> HOLDER_BITS).h);
+        if (m) H += hterm(D_LOCMIG, T, TupleHash(2).add(m & 1u).add((m >> 1) & 1u).h);   // NEXT-f2
+        if (e) H += hterm(D_LOC, T, TupleHash(2).add(e & HOLDER_MASK).add(e >> HOLDER_BITS).h);
     }
     __shared__ unsigned long long red[32];
     unsigned long long v = H;

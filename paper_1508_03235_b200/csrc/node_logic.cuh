@@ -106,15 +106,48 @@ __device__ __forceinline__ size_t loc_index(const Dev &S, uint32_t T)
     return (size_t)q * S.nloc + (h - S.n0);
 }
 
-// L2HIT: stamp update on a hit (R23)
-__device__ __forceinline__ bool l2_hit(const Dev &S, const NodeCtx &c, uint32_t T, uint64_t t)
+// NEXT-f2 "statistics counter ... last N accesses" (R45): the
+// ring of the last mig_hist accessor ids of line li (count / head in v.w)
+__device__ __forceinline__ void record_access(const Dev &S, size_t li, uint4 &v, uint32_t who)
+{
+    const uint32_t N = S.mig_hist;
+    if (!N) return;
+    uint32_t cnt = lw_count(v.w), head = lw_head(v.w);
+    if (cnt < N) {
+        S.l2h[li * N + (head + cnt) % N] = who;
+        ++cnt;
+    } else {
+        S.l2h[li * N + head] = who;
+        head = (head + 1u) % N;
+    }
+    v.w = lw_make(lw_state(v.w), cnt, head, lw_target(v.w));
+}
+
+// index of the valid line holding T in node c's slice, or -1
+__device__ __forceinline__ int l2_way(const Dev &S, const NodeCtx &c, uint32_t T)
+{
+    const uint4 *L = S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways;
+    for (uint32_t w = 0; w < S.ways; ++w) {
+        const uint4 v = L[w];
+        if (v.x == T + 1u && line_valid(v)) return (int)w;
+    }
+    return -1;
+}
+
+// L2HIT by accessor `who` (the owner for a local access, the requester of a
+// served RQ): stamp update (R23) and, with migration, the access record
+__device__ __forceinline__ bool l2_hit(const Dev &S, const NodeCtx &c, uint32_t T, uint64_t t, uint32_t who)
 {
     uint32_t set = T % S.sets;
-    uint4 *L = S.l2 + ((size_t)c.l * S.sets + set) * S.ways;
+    const size_t l0 = ((size_t)c.l * S.sets + set) * S.ways;
+    uint4 *L = S.l2 + l0;
     for (uint32_t w = 0; w < S.ways; ++w) {
         uint4 v = L[w];
-        if (v.x == T + 1u) {
-            L[w] = make_uint4(v.x, (uint32_t)t, (uint32_t)(t >> 32), 0u);
+        if (v.x == T + 1u && line_valid(v)) {
+            v.y = (uint32_t)t;
+            v.z = (uint32_t)(t >> 32);
+            record_access(S, l0 + w, v, who);
+            L[w] = v;
             return true;
         }
     }
@@ -127,6 +160,20 @@ __device__ __forceinline__ void ev_handler(const Dev &S, const Sink &K, uint32_t
     size_t i = loc_index(S, T);
     uint32_t e = S.loc[i];
     uint32_t h1 = e & HOLDER_MASK, pend = e >> HOLDER_BITS;
+    if (S.mig_hist) {
+        const uint32_t m = S.loc_mig[i];
+        if (m & 1u) {
+            if (h1 != src + 1u) {
+                // NEXT-f2 (R47): the migration target evicted T before its
+                // directory update arrived; the update leaves the entry empty
+                if (m & 2u) atomicOr(S.err, ERR_PROTO);
+                S.loc_mig[i] = (uint8_t)(m | 2u);
+                K.cnt(S, C_EVRCVD);
+                return;
+            }
+            S.loc_mig[i] = (uint8_t)(m & ~1u);   // the source evicted T before sending it: aborted
+        }
+    }
     if (h1 != src + 1u) atomicOr(S.err, ERR_EVHOLDER);
     if (pend > 0) --pend;
     else h1 = 0;
@@ -138,29 +185,41 @@ __device__ __forceinline__ void ev_handler(const Dev &S, const Sink &K, uint32_t
 static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
 {
     uint32_t set = T % S.sets;
-    uint4 *L = S.l2 + ((size_t)c.l * S.sets + set) * S.ways;
+    const size_t l0 = ((size_t)c.l * S.sets + set) * S.ways;
+    uint4 *L = S.l2 + l0;
+    if (S.mig_hist)   // NEXT-f2: a forwarding ghost of T itself is dropped (T lives here again)
+        for (uint32_t w = 0; w < S.ways; ++w) {
+            const uint4 v = L[w];
+            if (v.x == T + 1u && lw_state(v.w) == MS_FWD) L[w] = make_uint4(0, 0, 0, 0);
+        }
     uint32_t victim = 0;
     uint64_t best = ~0ull;
     bool found_invalid = false;
     uint4 vline = make_uint4(0, 0, 0, 0);
     for (uint32_t w = 0; w < S.ways; ++w) {
         uint4 v = L[w];
-        if (v.x == 0u) {
+        if (!line_valid(v)) {
             if (!found_invalid) { victim = w; vline = v; found_invalid = true; }
         } else if (!found_invalid) {
             uint64_t st = ((uint64_t)v.z << 32) | v.y;
             if (st < best) { best = st; victim = w; vline = v; }
         }
     }
-    if (vline.x != 0u) {
+    if (line_valid(vline)) {
         uint32_t V = vline.x - 1u;
         uint32_t hv = home_of(S, V);
         K.cnt(S, C_EVICTIONS);
-        K.cnt(S, C_EVSENT);
-        if (hv == c.n) ev_handler(S, K, V, c.n);
-        else enq(S, K, c, KEV, hv, V, 1u);
+        // NEXT-f2 (R49): a block already on its way to a migration target is
+        // dropped without an EV (the target's directory update takes over)
+        if (lw_state(vline.w) != MS_MIGSENT) {
+            K.cnt(S, C_EVSENT);
+            if (hv == c.n) ev_handler(S, K, V, c.n);
+            else enq(S, K, c, KEV, hv, V, 1u);
+        }
     }
-    L[victim] = make_uint4(T + 1u, (uint32_t)t, (uint32_t)(t >> 32), 0u);
+    uint4 nl = make_uint4(T + 1u, (uint32_t)t, (uint32_t)(t >> 32), 0u);
+    record_access(S, l0 + victim, nl, c.n);   // a fresh residency: the installing access (R45)
+    L[victim] = nl;
     K.cnt(S, C_INSTALLS);
 }
 
@@ -194,12 +253,15 @@ __device__ __forceinline__ void complete(const Dev &S, const Sink &K, NodeCtx &c
     set_mode(c, MIDLE, 0);
 }
 
-__device__ __forceinline__ void receive_ndr(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
+// core cold word w: install [0:2) (0 none, 1 install, 2 install and the
+// directory counted an EV of ours, NEXT-f2 R47) | rx << 2
+__device__ __forceinline__ void receive_ndr(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t, uint32_t payload)
 {
     if (core_mode(c.hot) != MWAITDIR) atomicOr(S.err, ERR_PROTO);
     K.cnt(S, C_MEMREQ);
     load_cold(S, c);
-    c.cold.w = (c.cold.w & ~1u) | 1u;          // install = 1
+    const uint32_t inst = (payload & NDR_NOINSTALL) ? 0u : (payload & NDR_PEND) ? 2u : 1u;
+    c.cold.w = (c.cold.w & ~3u) | inst;
     c.cold_dirty = true;
     set_mode(c, MMEMWAIT, t + S.mem_lat);
 }
@@ -248,26 +310,252 @@ static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint
     uint32_t kind, payload;
     if (h1 == 0u) {
         h1 = r + 1u; kind = KNDR; payload = T;
+    } else if (h1 == r + 1u && S.mig_hist && (S.loc_mig[i] & 1u)) {
+        // NEXT-f2 (R47): r sent T away and dropped its copy; the block is on
+        // its way to the target: r fetches from memory without installing
+        kind = KNDR; payload = T | NDR_NOINSTALL;
     } else if (h1 == r + 1u) {
         ++pend;
         if (pend > PEND_MAX) { atomicOr(S.err, ERR_PEND); pend = PEND_MAX; }
-        kind = KNDR; payload = T;
+        kind = KNDR; payload = T | (S.mig_hist ? NDR_PEND : 0u);
     } else {
         kind = KDR; payload = h1 - 1u;
     }
     S.loc[i] = h1 | (pend << HOLDER_BITS);
     if (r == c.n) {
-        if (kind == KNDR) receive_ndr(S, K, c, t);
+        if (kind == KNDR) receive_ndr(S, K, c, t, payload);
         else receive_dr(S, K, c, payload);
     } else {
         enq(S, K, c, kind, r, payload, 1u);
     }
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-f2: migration and redirection (Table I; SPEC
+// S:L226-243; DESIGN R44-R52).  Loopbacks (a message to the node
+// itself) are handled inline without flits (R51), written out without
+// recursion.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ctl_enq(const Dev &S, const Sink &K, NodeCtx &c, uint32_t to, uint32_t sub, uint32_t v,
+                                        uint32_t nfl = 1u)
+{
+    enq(S, K, c, KPROBE, to, ctl_word(sub, v), nfl);
+}
+
+// "If a remote node have accessed it mostly, then migration get triggered"
+// (SPEC should_migrate S:L235-243; R46): the node with the most
+// entries in line li's history (ties: lowest id) if it is not the holder h
+// and strictly ahead of h; else 0xFFFFFFFF
+static __device__ uint32_t mig_target(const Dev &S, size_t li, uint32_t w, uint32_t h)
+{
+    const uint32_t N = S.mig_hist, cnt = lw_count(w), head = lw_head(w);
+    const uint32_t *H = S.l2h + li * N;
+    uint32_t best = 0xFFFFFFFFu, bestc = 0, hc = 0;
+    for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t a = H[(head + i) % N];
+        uint32_t k = 0;
+        for (uint32_t j = 0; j < cnt; ++j) k += H[(head + j) % N] == a;
+        if (a == h) hc = k;
+        if (k > bestc || (k == bestc && a < best)) { best = a; bestc = k; }
+    }
+    return (best != 0xFFFFFFFFu && best != h && bestc > hc) ? best : 0xFFFFFFFFu;
+}
+
+// the B2 block (nfl_b2 flits, Table I: 16), enqueued as <= 8-flit parts (R50)
+__device__ __forceinline__ void send_block(const Dev &S, const Sink &K, NodeCtx &c, uint32_t R, uint32_t T)
+{
+    for (uint32_t left = S.nfl_b2; left;) {
+        const uint32_t k = left > 8u ? 8u : left;
+        ctl_enq(S, K, c, R, SUB_MIG, T, k);
+        left -= k;
+    }
+}
+
+// at home(T): a migration request from src; grant iff src holds T, no EV of T
+// is pending and no migration of T is in flight (R47)
+__device__ __forceinline__ bool dir_mr(const Dev &S, uint32_t T, uint32_t src)
+{
+    const size_t i = loc_index(S, T);
+    const uint32_t e = S.loc[i];
+    const bool ok = (e & HOLDER_MASK) == src + 1u && (e >> HOLDER_BITS) == 0u && !(S.loc_mig[i] & 1u);
+    if (ok) S.loc_mig[i] = 1u;
+    return ok;
+}
+
+// at the holder: grant -> send the block (if the line is still here), nack -> keep it
+static __device__ void src_grant(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, bool ok)
+{
+    const int w = l2_way(S, c, T);
+    if (!ok) K.cnt(S, C_MIGNACK);
+    if (w < 0) return;                      // evicted meanwhile: its EV aborts the transit
+    uint4 *L = S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways + w;
+    uint4 v = *L;
+    if (lw_state(v.w) != MS_MIGREQ) return;
+    const uint32_t R = lw_target(v.w);
+    if (ok) {
+        v.w = lw_make(MS_MIGSENT, lw_count(v.w), lw_head(v.w), R);
+        *L = v;
+        K.cnt(S, C_MIGS);
+        send_block(S, K, c, R, T);
+    } else {
+        v.w = lw_make(MS_NORMAL, lw_count(v.w), lw_head(v.w), 0u);
+        *L = v;
+    }
+}
+
+// at the old holder: "source packet invalidates its copy", keeping a
+// forwarding ghost (tag, target) for redirection (R48)
+__device__ __forceinline__ void src_inv(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T)
+{
+    K.cnt(S, C_INVAL);
+    const int w = l2_way(S, c, T);
+    if (w < 0) return;
+    uint4 *L = S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways + w;
+    const uint4 v = *L;
+    if (lw_state(v.w) != MS_MIGSENT) return;
+    *L = make_uint4(v.x, 0u, 0u, lw_make(MS_FWD, 0u, 0u, lw_target(v.w)));
+}
+
+// at home(T): the directory update from the new holder src (R47)
+static __device__ void dir_du(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t src)
+{
+    const size_t i = loc_index(S, T);
+    const uint32_t m = S.loc_mig[i];
+    if (!(m & 1u)) { atomicOr(S.err, ERR_PROTO); return; }
+    const uint32_t e = S.loc[i];
+    const uint32_t h = (e & HOLDER_MASK) - 1u;
+    S.loc_mig[i] = 0u;
+    K.cnt(S, C_DIRUPD);
+    S.loc[i] = ((m & 2u) ? 0u : src + 1u) | (e & ~HOLDER_MASK);
+    if (h == c.n) src_inv(S, K, c, T);
+    else ctl_enq(S, K, c, h, SUB_INV, T);
+}
+
+// a flit of an inbound block; the last one installs it and updates the directory
+static __device__ void dst_mig_flit(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
+{
+    uint2 *X = S.migrx + (size_t)c.l * 4u;
+    int k = -1;
+    for (int j = 0; j < 4; ++j) if (X[j].y && X[j].x == T) k = j;
+    if (k < 0)
+        for (int j = 0; j < 4 && k < 0; ++j) if (!X[j].y) k = j;
+    if (k < 0) { atomicOr(S.err, ERR_MIGRX); return; }
+    const uint32_t cnt = (X[k].y ? X[k].y : 0u) + 1u;
+    if (cnt < S.nfl_b2) { X[k] = make_uint2(T, cnt); return; }
+    X[k] = make_uint2(0u, 0u);
+    if (l2_way(S, c, T) >= 0) { atomicOr(S.err, ERR_PROTO); return; }
+    install(S, K, c, T, t);
+    K.cnt(S, C_MIGINST);
+    const uint32_t home = home_of(S, T);
+    if (home == c.n) dir_du(S, K, c, T, c.n);
+    else ctl_enq(S, K, c, home, SUB_DU, T);
+}
+
+// after an RQ served at this node: maybe start a migration (R46, R47)
+static __device__ void maybe_migrate(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, int w)
+{
+    const size_t li = ((size_t)c.l * S.sets + T % S.sets) * S.ways + w;
+    uint4 v = S.l2[li];
+    if (lw_state(v.w) != MS_NORMAL) return;
+    const uint32_t R = mig_target(S, li, v.w, c.n);
+    if (R == 0xFFFFFFFFu) return;
+    v.w = lw_make(MS_MIGREQ, lw_count(v.w), lw_head(v.w), R);
+    S.l2[li] = v;
+    K.cnt(S, C_MIGREQ);
+    const uint32_t home = home_of(S, T);
+    if (home == c.n) src_grant(S, K, c, T, dir_mr(S, T, c.n));
+    else ctl_enq(S, K, c, home, SUB_MR, T);
+}
+
+// RQ for T from requester r at this node (Fig. 4 step 4): serve from
+// the slice (RA), else redirect through a forwarding ghost (R48), else
+// TRAP.  r == c.n only for a redirection to the requester itself,
+// served inline (R51).
+static __device__ void serve_rq(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t r, uint64_t t)
+{
+    K.cnt(S, C_REQRCVD);
+    if (l2_hit(S, c, T, t, r)) {
+        K.cnt(S, C_REPSENT);
+        if (r == c.n) {
+            K.cnt(S, C_REPRCVD);
+            l1_fill(S, K, c, T, c.n, t);
+            complete(S, K, c, t);
+        } else {
+            enq(S, K, c, KRA, r, T, S.nfl_ra);
+        }
+        if (S.mig_hist) maybe_migrate(S, K, c, T, l2_way(S, c, T));
+        return;
+    }
+    if (S.mig_hist && r != c.n) {
+        const uint4 *L = S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways;
+        for (uint32_t w = 0; w < S.ways; ++w) {
+            const uint4 v = L[w];
+            if (v.x == T + 1u && lw_state(v.w) == MS_FWD) {
+                K.cnt(S, C_REDIR);
+                ctl_enq(S, K, c, r, SUB_RR, lw_target(v.w));
+                return;
+            }
+        }
+    }
+    K.cnt(S, C_TRAPSENT);
+    if (r == c.n) {
+        K.cnt(S, C_TRAPRCVD);
+        K.cnt(S, C_MEMREQ);
+        load_cold(S, c);
+        c.cold.w &= ~3u;
+        c.cold_dirty = true;
+        set_mode(c, MMEMWAIT, t + S.mem_lat);
+    } else {
+        enq(S, K, c, KTRAP, r, T, 1u);
+    }
+}
+
+// a migration / redirection message (sub, v) from src delivered here (R47, R48)
+static __device__ void ctl_deliver(const Dev &S, const Sink &K, NodeCtx &c, uint32_t sub, uint32_t v, uint32_t src,
+                                   uint64_t t)
+{
+    switch (sub) {
+    case SUB_MR: ctl_enq(S, K, c, src, dir_mr(S, v, src) ? SUB_MG : SUB_MN, v); break;
+    case SUB_MG: src_grant(S, K, c, v, true); break;
+    case SUB_MN: src_grant(S, K, c, v, false); break;
+    case SUB_MIG: dst_mig_flit(S, K, c, v, t); break;
+    case SUB_DU: dir_du(S, K, c, v, src); break;
+    case SUB_INV: src_inv(S, K, c, v); break;
+    case SUB_RR:   // "Reply redirection" (Table I; R48): ask the new holder v
+        if (core_mode(c.hot) != MWAITDATA) atomicOr(S.err, ERR_PROTO);
+        K.cnt(S, C_RRRCVD);
+        K.cnt(S, C_REQMADE);
+        load_cold(S, c);
+        if (v == c.n) serve_rq(S, K, c, c.cold.z, c.n, t);
+        else enq(S, K, c, KRQ, v, c.cold.z, 1u);
+        break;
+    default: atomicOr(S.err, ERR_PROTO); break;
+    }
+}
+
+// MEMWAIT over with an install pending; NEXT-f2 (R47): if the block
+// migrated here meanwhile there is no second copy, and if the directory
+// counted an EV of ours that does not exist, one is sent to even it
+static __device__ void mem_fill(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t)
+{
+    load_cold(S, c);
+    const uint32_t T = c.cold.z;
+    if (S.mig_hist && l2_way(S, c, T) >= 0) {
+        if ((c.cold.w & 3u) == 2u) {
+            const uint32_t hv = home_of(S, T);
+            K.cnt(S, C_EVSENT);
+            if (hv == c.n) ev_handler(S, K, T, c.n);
+            else enq(S, K, c, KEV, hv, T, 1u);
+        }
+        return;
+    }
+    install(S, K, c, T, t);
+}
+
 // The local L2 part of an access (Fig. 4): hit, else the directory
 static __device__ void l2_access(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
 {
-    if (l2_hit(S, c, T, t)) {
+    if (l2_hit(S, c, T, t, c.n)) {
         K.cnt(S, C_L2HIT);
         if (S.l2_hit_lat == 0u) {
             l1_fill(S, K, c, T, c.n, t);
@@ -378,7 +666,7 @@ __device__ __forceinline__ void predraw(const Dev &S, NodeCtx &c, uint64_t t1)
     if (!S.gen || S.has_script || S.mode == 0u) return;
     const uint32_t mode = core_mode(c.hot);
     const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t1) & 0x1FFFFFFFu) == 0u);
-    if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
+    if (expiring && mode == MMEMWAIT && (c.cold.w & 3u)) prefetch_l1(set_ptr(S, c, c.cold.z));
     if (mode == MIDLE || expiring) {
         c.nd_fire = draw(S, c, t1, c.nd_val);
         c.nd_t = (uint32_t)t1;
@@ -421,7 +709,7 @@ __device__ __forceinline__ void phase1_lspd(const Dev &S, const Sink &K, NodeCtx
     }
     if ((mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {
         load_cold(S, c);
-        if (mode == MMEMWAIT && (c.cold.w & 1u)) install(S, K, c, c.cold.z, t);
+        if (mode == MMEMWAIT && (c.cold.w & 3u)) mem_fill(S, K, c, t);
         l1_fill(S, K, c, c.cold.z, c.n, t);       // local L2 hit or memory fill: supplied locally (R42)
         complete(S, K, c, t);
         mode = MIDLE;
@@ -455,7 +743,7 @@ __device__ __forceinline__ void phase1_lspd_win(const Dev &S, const Sink &K, Nod
     }
     if ((mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)t) & 0x1FFFFFFFu) == 0u)) {
         load_cold(S, c);
-        if (mode == MMEMWAIT && (c.cold.w & 1u)) install(S, K, c, c.cold.z, t);
+        if (mode == MMEMWAIT && (c.cold.w & 3u)) mem_fill(S, K, c, t);
         if (L1) l1_fill(S, K, c, c.cold.z, c.n, t);   // local L2 hit or memory fill: supplied locally (R42)
         complete(S, K, c, t);
         mode = MIDLE;
@@ -628,8 +916,9 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
     K.hist(S, 0, (uint32_t)t - f.z);
     K.hist(S, 1, f_age(f));
     switch (f_kind(f)) {
-    case KPROBE:
-        K.cnt(S, C_PROBES);
+    case KPROBE:   // = the migration / redirection messages in LSPD mode (R50)
+        if (S.mode != 0u) ctl_deliver(S, K, c, f.w >> 28, f.w & 0x0FFFFFFFu, f_src(f), t);
+        else K.cnt(S, C_PROBES);
         break;
     case KDA:
         dir_service(S, K, c, f.w, f_src(f), t);
@@ -638,30 +927,23 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
         receive_dr(S, K, c, f.w);
         break;
     case KNDR:
-        receive_ndr(S, K, c, t);
+        receive_ndr(S, K, c, t, f.w);
         break;
     case KRQ:
-        K.cnt(S, C_REQRCVD);
-        if (l2_hit(S, c, f.w, t)) {
-            K.cnt(S, C_REPSENT);
-            enq(S, K, c, KRA, f_src(f), f.w, S.nfl_ra);
-        } else {
-            K.cnt(S, C_TRAPSENT);
-            enq(S, K, c, KTRAP, f_src(f), f.w, 1u);
-        }
+        serve_rq(S, K, c, f.w, f_src(f), t);
         break;
     case KRA: {
         if (core_mode(c.hot) != MWAITDATA) atomicOr(S.err, ERR_PROTO);
         load_cold(S, c);
-        uint32_t rx = (c.cold.w >> 1) + 1u;
+        uint32_t rx = (c.cold.w >> 2) + 1u;
         if (rx == S.nfl_ra) {
-            c.cold.w &= 1u;
+            c.cold.w &= 3u;
             c.cold_dirty = true;
             K.cnt(S, C_REPRCVD);
             l1_fill(S, K, c, c.cold.z, f_src(f), t);   // supplied by the holder's slice (R42)
             complete(S, K, c, t);
         } else {
-            c.cold.w = (c.cold.w & 1u) | (rx << 1);
+            c.cold.w = (c.cold.w & 3u) | (rx << 2);
             c.cold_dirty = true;
         }
         break;
@@ -671,7 +953,7 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
         K.cnt(S, C_TRAPRCVD);
         K.cnt(S, C_MEMREQ);
         load_cold(S, c);
-        c.cold.w &= ~1u;                          // install = 0 (R16)
+        c.cold.w &= ~3u;                          // install = 0 (R16)
         c.cold_dirty = true;
         set_mode(c, MMEMWAIT, t + S.mem_lat);
         break;

@@ -136,11 +136,13 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    for (size_t i = 0; i < sizeof c->reserved / sizeof c->reserved[0]; ++i)
-        if (c->reserved[i]) return fail(NOC_EINVAL, "reserved fields must be 0");
     if (c->inject_mode > 1) return fail(NOC_EINVAL, "inject_mode out of range");
     if (c->age_base > AGE_MAX) return fail(NOC_EINVAL, "age_base > 65535 (R32)");
     if (c->band_streams > 1) return fail(NOC_EINVAL, "band_streams must be 0 or 1");
+    if (c->mig_hist > 16) return fail(NOC_EINVAL, "mig_hist must be 0..16");
+    if (c->mig_hist && (c->mode != NOC_MODE_LSPD || c->nfl_b2 < 1 || c->nfl_b2 > 16 ||
+                        (uint64_t)c->tags_per_node * c->mesh_w * c->mesh_h > (1ull << 28)))
+        return fail(NOC_EINVAL, "migration needs LSPD mode, nfl_b2 1..16 and a tag space <= 2^28 (R50)");
     if (c->band_streams && (c->bands < 2 || c->world_size > 1 ||
                             (c->engine != NOC_ENGINE_TILED && c->engine != NOC_ENGINE_AUTO)))
         return fail(NOC_EINVAL, "band_streams needs bands >= 2 in one process and the TILED engine");
@@ -212,6 +214,8 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.l1_miss_lat = cfg->l1_miss_lat;
     D.inject_mode = cfg->inject_mode;
     D.age_base = cfg->age_base;
+    D.mig_hist = cfg->mode == NOC_MODE_LSPD ? cfg->mig_hist : 0u;
+    D.nfl_b2 = cfg->nfl_b2;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
@@ -248,6 +252,11 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
         if (D.dir_mode) D.loc_n = (D.dir_node >= D.n0 && D.dir_node < D.n0 + D.nloc) ? (uint64_t)D.tpn * D.N : 0u;
         else D.loc_n = (uint64_t)D.tpn * n;
         if ((rc = dalloc(s, &D.loc, (size_t)D.loc_n))) return rc;
+        if (D.mig_hist) {   // NEXT-f2 state: accessor rings, directory transit flags, inbound reassembly
+            if ((rc = dalloc(s, &D.l2h, n * D.sets * D.ways * (size_t)D.mig_hist))) return rc;
+            if ((rc = dalloc(s, &D.loc_mig, (size_t)D.loc_n))) return rc;
+            if ((rc = dalloc(s, &D.migrx, n * 4u))) return rc;
+        }
         s->loc_bytes += s->bytes - b0;
     }
     // script events of this band's nodes, per node ordered by (cycle, input order)
@@ -546,6 +555,7 @@ static int check_err(noc_sim *s)
             return fail(NOC_ECUDA, b);
         }
         if (err & ERR_DROP) return fail(NOC_EOVERFLOW, "send FIFO overflow in LSPD mode (R21: a dropped protocol message)");
+        if (err & ERR_MIGRX) return fail(NOC_EOVERFLOW, "more than 4 inbound migrations at one node (R52)");
         if (err & (ERR_AGE | ERR_PEND)) return fail(NOC_EOVERFLOW, "field width exceeded (flit age, lifetime or pend)");
         return fail(NOC_ECUDA, "model assertion failed on device (protocol / EV holder)");
     }
@@ -762,6 +772,8 @@ extern "C" int noc_sim_stats(noc_sim *s, noc_sim_counters *out, uint64_t *hl, ui
         out->l1_misses = (int64_t)c[C_L1MISS];
         out->wb_sent = (int64_t)c[C_WBSENT];
         out->wb_received = (int64_t)c[C_WBRCVD];
+        int64_t *mg = &out->mig_requests;
+        for (int k = 0; k < 8; ++k) mg[k] = (int64_t)c[C_MIGREQ + k];
     }
     uint64_t *hs[3] = {hl, hd, ha};
     for (int k = 0; k < 3; ++k)

@@ -445,7 +445,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         if (!active) return false;
         const uint32_t mode = core_mode(c.hot);
         const bool expiring = (mode == ML2WAIT || mode == MMEMWAIT) && (((c.hot ^ (uint32_t)tn) & 0x1FFFFFFFu) == 0u);
-        if (expiring && mode == MMEMWAIT && (c.cold.w & 1u)) prefetch_l1(set_ptr(S, c, c.cold.z));
+        if (expiring && mode == MMEMWAIT && (c.cold.w & 3u)) prefetch_l1(set_ptr(S, c, c.cold.z));
         return (mode == MIDLE || expiring) && (uint32_t)tn - wbase >= 32u;
     };
     // LSPD with draw windows: Phase 1 of a node has work only at its next due
@@ -739,7 +739,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 const bool due = active && stn == wake;
                 const bool need = due && stn - wbase >= 32u;
                 // the set a memory fill installs into one cycle ahead (L1 prefetch)
-                if (active && stn + 1u == wake && core_mode(c.hot) == MMEMWAIT && (c.cold.w & 1u))
+                if (active && stn + 1u == wake && core_mode(c.hot) == MMEMWAIT && (c.cold.w & 3u))
                     prefetch_l1(set_ptr(S, c, c.cold.z));
                 if (__any_sync(FULL, need)) {
                     TRACE_EV(8u);

@@ -65,10 +65,12 @@ def c1b(seed=1, **kw):
 
 
 def lspd(w, h, seed=1, lam=0.05, **kw):
-    """LSPD with the Table III rows 3-4 slice (32 sets x 2 ways x 32 B)."""
+    """LSPD with the Table III rows 3-4 slice (32 sets x 2 ways x 32 B) by default."""
     kw.setdefault("p_priv", 0.5)
     kw.setdefault("sendq_cap", 32)
-    return make(mesh_w=w, mesh_h=h, mode=MODE_LSPD, l2_sets=32, l2_ways=2, lam=lam, seed=seed, **kw)
+    kw.setdefault("l2_sets", 32)
+    kw.setdefault("l2_ways", 2)
+    return make(mesh_w=w, mesh_h=h, mode=MODE_LSPD, lam=lam, seed=seed, **kw)
 
 
 def c2(seed=1, **kw):

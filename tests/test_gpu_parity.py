@@ -484,3 +484,47 @@ def test_maximum_sizes(cfg, cycles):
     AUTO engine against the oracle."""
     g, o = both(cfg, cycles)
     assert_same(g, o)
+
+
+MIG_CASES = {
+    "c1b_mig1": W.c1b(mig_hist=1, seed=2),
+    "lspd16_mig2_b2x3": W.lspd(16, 16, lam=0.3, mig_hist=2, nfl_b2=3, sendq_cap=128, l2_sets=4, tags_per_node=16,
+                               priv_tags=8, mem_lat=20),
+    "stress5x6": W.make(mesh_w=5, mesh_h=6, mode=W.MODE_LSPD, l2_sets=2, l2_ways=2, lam=0.7, p_priv=0.0,
+                        sendq_cap=512, mig_hist=3, nfl_b2=16, tags_per_node=4, priv_tags=1, mem_lat=3, seed=9),
+    "central_l1_mig": W.lspd(12, 10, lam=0.3, mig_hist=4, nfl_b2=16, dir_mode=W.DIR_CENTRAL, dir_node=55,
+                             sendq_cap=256, l1_sets=2, l1_ways=1, tags_per_node=8, priv_tags=4, mem_lat=10),
+}
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("name", sorted(MIG_CASES))
+def test_migration_and_redirection(name, engine):
+    """NEXT-f2 (R44-R52): accessor histories, home-granted migrations of
+    16-flit blocks, directory updates, invalidations, forwarding ghosts and
+    redirections on every engine, bit-exact against the oracle, then drained
+    (every migration completed)."""
+    cfg = MIG_CASES[name]
+    g, o = both(cfg, 3000, engine, drain=200000)
+    assert_same(g, o)
+    st = g.stats()[0]
+    assert st["migrations"] > 0 and st["migrations"] == st["mig_installs"] == st["dir_updates"]
+    g.run(700)
+    o.run(700)
+    assert_same(g, o)
+
+
+def test_migration_c3_and_bands():
+    """C3 with migration (1-entry histories: a remote reader outvotes the holder, 16-flit blocks) on the default
+    engine, and a 22x19 mesh with migration over 3 virtual bands."""
+    cfg = W.c3(mig_hist=1)
+    g, o = both(cfg, 1500)
+    assert_same(g, o)
+    assert g.stats()[0]["migrations"] > 0
+    cfg = W.lspd(22, 19, lam=0.3, mig_hist=3, tags_per_node=8, priv_tags=4, sendq_cap=256)
+    for engine in (nb.ENGINE_TILED, nb.ENGINE_PERSIST):
+        g = nb.NocSim(cfg, bands=3, engine=engine)
+        o = Oracle(cfg)
+        g.run(1500)
+        o.run(1500)
+        assert_same(g, o)
