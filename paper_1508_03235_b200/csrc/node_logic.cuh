@@ -108,11 +108,15 @@ __device__ __forceinline__ size_t loc_index(const Dev &S, uint32_t T)
 
 // NEXT-f2 "statistics counter ... last N accesses" (R45): the
 // ring of the last mig_hist accessor ids of line li (count / head in v.w)
+static __device__ __noinline__ uint32_t record_ring(const Dev &S, size_t li, uint32_t w, uint32_t who);
 __device__ __forceinline__ void record_access(const Dev &S, size_t li, uint4 &v, uint32_t who)
 {
+    if (S.mig_hist) v.w = record_ring(S, li, v.w, who);
+}
+static __device__ __noinline__ uint32_t record_ring(const Dev &S, size_t li, uint32_t vw, uint32_t who)
+{
     const uint32_t N = S.mig_hist;
-    if (!N) return;
-    uint32_t cnt = lw_count(v.w), head = lw_head(v.w);
+    uint32_t cnt = lw_count(vw), head = lw_head(vw);
     if (cnt < N) {
         S.l2h[li * N + (head + cnt) % N] = who;
         ++cnt;
@@ -120,7 +124,7 @@ __device__ __forceinline__ void record_access(const Dev &S, size_t li, uint4 &v,
         S.l2h[li * N + head] = who;
         head = (head + 1u) % N;
     }
-    v.w = lw_make(lw_state(v.w), cnt, head, lw_target(v.w));
+    return lw_make(lw_state(vw), cnt, head, lw_target(vw));
 }
 
 // index of the valid line holding T in node c's slice, or -1
@@ -182,16 +186,21 @@ __device__ __forceinline__ void ev_handler(const Dev &S, const Sink &K, uint32_t
 }
 
 // INSTALL (victim: first invalid, else min stamp, ties lowest way, R23)
+// NEXT-f2: a forwarding ghost of T in this set is dropped
+static __device__ __noinline__ void drop_ghost(const Dev &S, uint4 *L, uint32_t T)
+{
+    for (uint32_t w = 0; w < S.ways; ++w) {
+        const uint4 v = L[w];
+        if (v.x == T + 1u && lw_state(v.w) == MS_FWD) L[w] = make_uint4(0, 0, 0, 0);
+    }
+}
+
 static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint64_t t)
 {
     uint32_t set = T % S.sets;
     const size_t l0 = ((size_t)c.l * S.sets + set) * S.ways;
     uint4 *L = S.l2 + l0;
-    if (S.mig_hist)   // NEXT-f2: a forwarding ghost of T itself is dropped (T lives here again)
-        for (uint32_t w = 0; w < S.ways; ++w) {
-            const uint4 v = L[w];
-            if (v.x == T + 1u && lw_state(v.w) == MS_FWD) L[w] = make_uint4(0, 0, 0, 0);
-        }
+    if (S.mig_hist) drop_ghost(S, L, T);   // NEXT-f2: T lives here again
     uint32_t victim = 0;
     uint64_t best = ~0ull;
     bool found_invalid = false;
@@ -467,6 +476,21 @@ static __device__ void maybe_migrate(const Dev &S, const Sink &K, NodeCtx &c, ui
     else ctl_enq(S, K, c, home, SUB_MR, T);
 }
 
+// a forwarding ghost of T here: redirect the requester r to the new holder (R48)
+static __device__ bool redirect(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t r)
+{
+    const uint4 *L = S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways;
+    for (uint32_t w = 0; w < S.ways; ++w) {
+        const uint4 v = L[w];
+        if (v.x == T + 1u && lw_state(v.w) == MS_FWD) {
+            K.cnt(S, C_REDIR);
+            ctl_enq(S, K, c, r, SUB_RR, lw_target(v.w));
+            return true;
+        }
+    }
+    return false;
+}
+
 // RQ for T from requester r at this node (Fig. 4 step 4): serve from
 // the slice (RA), else redirect through a forwarding ghost (R48), else
 // TRAP.  r == c.n only for a redirection to the requester itself,
@@ -486,17 +510,7 @@ static __device__ void serve_rq(const Dev &S, const Sink &K, NodeCtx &c, uint32_
         if (S.mig_hist) maybe_migrate(S, K, c, T, l2_way(S, c, T));
         return;
     }
-    if (S.mig_hist && r != c.n) {
-        const uint4 *L = S.l2 + ((size_t)c.l * S.sets + T % S.sets) * S.ways;
-        for (uint32_t w = 0; w < S.ways; ++w) {
-            const uint4 v = L[w];
-            if (v.x == T + 1u && lw_state(v.w) == MS_FWD) {
-                K.cnt(S, C_REDIR);
-                ctl_enq(S, K, c, r, SUB_RR, lw_target(v.w));
-                return;
-            }
-        }
-    }
+    if (S.mig_hist && r != c.n && redirect(S, K, c, T, r)) return;
     K.cnt(S, C_TRAPSENT);
     if (r == c.n) {
         K.cnt(S, C_TRAPRCVD);

@@ -567,6 +567,7 @@ static void set_gen(noc_sim *s, uint32_t gen)
     for (int k = 0; k < s->nb; ++k) {
         s->D[k].gen = gen;
         s->set.d[k].gen = gen;
+        s->bset[k].d[0].gen = gen;   // virtual ranks: each band's own launch set
     }
 }
 
