@@ -1,0 +1,10 @@
+# GPU tests + smoke + default bench + launch list of the bench (one gpurun call)
+cd $GRAFT_REPO_ROOT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --fresh 0 > gpurun_out/bench_ncu.log 2>&1
+timeout ${1:-2400} python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gputest.log 2>&1
+echo "rc=$?" >> gpurun_out/gputest.log
+tail -40 gpurun_out/gputest.log
+tail -3 gpurun_out/bench.log gpurun_out/smoke.log

@@ -73,4 +73,11 @@ for nm, msk in (("boundary", bnd), ("interior", ~bnd)):
     print("%s warps (p50 p90 mean clk from cycle start): ext done %s | published %s | phase3 done %s | "
           "phase1 done %s | barrier %s" % (nm, q(bx), q(pubw.reshape(arr.shape)), q(p3w.reshape(arr.shape)),
                                           q(p1w.reshape(arr.shape)), q(arr)))
+for par in (0, 1):
+    sel = (np.arange(TRACE_CYC - 1) % 2) == par
+    print("cycles with cc %% 2 == %d: CTA cycle median %d p90 %d; boundary ext done p50 %d p90 %d; interior phase1-done p50 %d p90 %d; boundary barrier p50 %d; interior barrier p50 %d" % (
+        par, np.median(clen[sel]), np.percentile(clen[sel], 90),
+        np.percentile(bx[:-1][sel][bnd[:-1][sel]], 50), np.percentile(bx[:-1][sel][bnd[:-1][sel]], 90),
+        np.percentile(p1w.reshape(arr.shape)[:-1][sel][~bnd[:-1][sel]], 50), np.percentile(p1w.reshape(arr.shape)[:-1][sel][~bnd[:-1][sel]], 90),
+        np.median(arr[:-1][sel][bnd[:-1][sel]]), np.median(arr[:-1][sel][~bnd[:-1][sel]])))
 print("last warp is a boundary warp in %.1f%% of CTA-cycles" % (100 * ((lastev >> 7) & 1).mean()))
