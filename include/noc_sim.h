@@ -121,8 +121,11 @@ typedef struct noc_sim_config {
     uint32_t l1_miss_lat;      /* "L1 miss cycle" countdown, 1 .. 2^29-1 */
     uint32_t inject_mode;      /* 0: R7 (inject only into a free input port);
                                   1: NEXT-f4, a flit that will eject frees its
-                                  input port for the same cycle.
-                                  Not supported by NOC_ENGINE_TILED4          */
+                                  input port for the same cycle;
+                                  2: NEXT-f4 fill-all, queued flits fill every
+                                  free input port, oldest-queued first (SPEC
+                                  S:L145; DESIGN R53).
+                                  1 and 2 are not supported by NOC_ENGINE_TILED4 */
     uint32_t age_base;         /* test knob: injected flits start at this age
                                   instead of 0; 0 = the paper's model,
                                   <= 65535.  Shifts every age equally (ranking

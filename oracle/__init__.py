@@ -94,6 +94,9 @@ def lib():
         L.orc_arbitrate.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_int),
                                     C.POINTER(C.c_uint64)]
+        L.orc_arbitrate_ex.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_uint64)]
         L.orc_links_occupied.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
         L.orc_links_occupied.restype = C.c_int64
         L.orc_fifo_packets.argtypes = [C.c_void_p]
@@ -144,17 +147,20 @@ def philox(key, ctr):
 
 
 def arbitrate(mesh_w, mesh_h, node, prio, flits, route=0):
-    """One router decision.  flits = [(dst, src, age, inj), ...].
+    """One router decision.  flits = [(dst, src, age, inj), ...] or
+    [(dst, src, age, inj, fid, kind, payload), ...] (the last three break ties
+    between flits one node injected in the same cycle, R53).
     Returns ([port...], [age_after...]); port 0..3 = N,S,E,W, 4 = eject.
     route: 0 = PMDR (R3, R5), 1 = strict XY with N,E,S,W deflection (NEXT-f4)."""
     nf = len(flits)
-    arr = (C.c_uint64 * (4 * max(nf, 1)))()
+    k = 7 if nf and len(flits[0]) == 7 else 4
+    arr = (C.c_uint64 * (k * max(nf, 1)))()
     for i, f in enumerate(flits):
-        for j in range(4):
-            arr[4 * i + j] = f[j]
+        for j in range(k):
+            arr[k * i + j] = f[j]
     ports = (C.c_int * 5)()
     ages = (C.c_uint64 * 5)()
-    rc = lib().orc_arbitrate(mesh_w, mesh_h, node, prio, route, nf, arr, ports, ages)
+    rc = lib().orc_arbitrate_ex(mesh_w, mesh_h, node, prio, route, nf, k, arr, ports, ages)
     if rc != 0:
         raise ValueError("more flits than router degree")
     return list(ports[:nf]), list(ages[:nf])

@@ -778,14 +778,21 @@ static void phase1(orc_sim *s, uint32_t n)
  * If there is a conflict it simply deflect to any free port except the
  * ejection port."
  * ---------------------------------------------------------------------- */
-typedef struct { uint32_t dst, src; uint64_t age, inj; } ArbFlit;
+typedef struct { uint32_t dst, src; uint64_t age, inj; uint32_t fid, kind, payload; } ArbFlit;
 
-/* 1 if a ranks strictly before b (R1, R2) */
+/* 1 if a ranks strictly before b (R1, R2).  Equal (age, inj, src) happens
+ * only for flits one node injected in the same cycle (fill-all injection,
+ * R53): they rank by fid, kind, dst, payload ascending; flits equal in all of
+ * these are identical and either order gives the same state */
 static int ranks_before(uint32_t prio, const ArbFlit *a, const ArbFlit *b)
 {
     if (prio == ORC_PRIO_DEFLECT && a->age != b->age) return a->age > b->age;
     if (a->inj != b->inj) return a->inj < b->inj;
-    return a->src < b->src;
+    if (a->src != b->src) return a->src < b->src;
+    if (a->fid != b->fid) return a->fid < b->fid;
+    if (a->kind != b->kind) return a->kind < b->kind;
+    if (a->dst != b->dst) return a->dst < b->dst;
+    return a->payload < b->payload;
 }
 
 /* Router decision for flits F[0..nf-1] at node n.  Writes port[i] and
@@ -860,21 +867,33 @@ static int arbitrate(uint32_t W, uint32_t H, uint32_t n, uint32_t prio, uint32_t
     return 0;
 }
 
-int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
-                  uint32_t nf, const uint64_t *flits, int *out_port, uint64_t *out_age)
+int orc_arbitrate_ex(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
+                     uint32_t nf, uint32_t stride, const uint64_t *flits, int *out_port, uint64_t *out_age)
 {
-    ArbFlit F[5] = {{0, 0, 0, 0}};
+    ArbFlit F[5] = {{0, 0, 0, 0, 0, 0, 0}};
     int defl[5];
-    if (nf > 5) return -1;
+    if (nf > 5 || (stride != 4 && stride != 7)) return -1;
     for (uint32_t i = 0; i < nf; ++i) {
-        F[i].dst = (uint32_t)flits[4 * i + 0];
-        F[i].src = (uint32_t)flits[4 * i + 1];
-        F[i].age = flits[4 * i + 2];
-        F[i].inj = flits[4 * i + 3];
+        const uint64_t *v = flits + (size_t)stride * i;
+        F[i].dst = (uint32_t)v[0];
+        F[i].src = (uint32_t)v[1];
+        F[i].age = v[2];
+        F[i].inj = v[3];
+        if (stride == 7) {
+            F[i].fid = (uint32_t)v[4];
+            F[i].kind = (uint32_t)v[5];
+            F[i].payload = (uint32_t)v[6];
+        }
     }
     if (arbitrate(mesh_w, mesh_h, node, prio, route, nf, F, out_port, defl) != 0) return -1;
     for (uint32_t i = 0; i < nf; ++i) out_age[i] = F[i].age + (uint64_t)defl[i];
     return 0;
+}
+
+int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
+                  uint32_t nf, const uint64_t *flits, int *out_port, uint64_t *out_age)
+{
+    return orc_arbitrate_ex(mesh_w, mesh_h, node, prio, route, nf, 4, flits, out_port, out_age);
 }
 
 static void phase2(orc_sim *s, uint32_t n)
@@ -893,12 +912,15 @@ static void phase2(orc_sim *s, uint32_t n)
         }
     }
     /* injection: one flit per cycle through InFromProc, only if a free input
-     * port exists (R7, R8); under the NEXT-f4 mode (R43) a flit
-     * that will eject frees its input port for the same cycle */
+     * port exists (R7, R8); under the NEXT-f4 mode 1 (R43) a flit
+     * that will eject frees its input port for the same cycle;
+     * under mode 2 (R53) queued flits fill every free input port, oldest-queued
+     * first, all injected this cycle (R8) */
     int frees = 0;
-    if (s->cfg.inject_mode)
+    if (s->cfg.inject_mode == 1)
         for (uint32_t i = 0; i < nf; ++i) frees |= F[i].dst == n;
-    if ((int)nf - frees < deg && c->count > 0) {
+    const uint32_t max_inj = s->cfg.inject_mode == 2 ? 4u : 1u;
+    for (uint32_t k = 0; k < max_inj && (int)nf - frees < deg && c->count > 0; ++k) {
         Packet *p = &c->fifo[c->head];
         Flit f;
         f.present = 1;
@@ -919,6 +941,7 @@ static void phase2(orc_sim *s, uint32_t n)
     if (nf == 0) return;
     for (uint32_t i = 0; i < nf; ++i) {
         A[i].dst = F[i].dst; A[i].src = F[i].src; A[i].age = F[i].age; A[i].inj = F[i].inj;
+        A[i].fid = F[i].fid; A[i].kind = F[i].kind; A[i].payload = F[i].payload;
         if (s->t - F[i].inj > LIFE_MAX) fail(s, ORC_EOVERFLOW, "flit lifetime overflow");
     }
     if (arbitrate(s->W, s->H, n, s->cfg.prio, s->cfg.route, nf, A, port, defl) != 0) {
@@ -1100,7 +1123,7 @@ int orc_create(const orc_config *cfg, orc_sim **out)
     if (W < 2 || H < 2 || W > 2048 || H > 2048 || (uint64_t)W * H > (1u << 21)) {
         set_err("mesh must be 2..2048 per side and at most 2^21 nodes"); return ORC_EINVAL;
     }
-    if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1 || cfg->inject_mode > 1) {
+    if (cfg->mode > 1 || cfg->prio > 1 || cfg->route > 1 || cfg->inject_mode > 2) {
         set_err("bad mode/prio/route/inject_mode");
         return ORC_EINVAL;
     }

@@ -68,7 +68,8 @@ typedef struct {
     uint32_t dir_node;           /* dir_mode 1: the node holding the directory */
     uint32_t l1_sets, l1_ways;   /* NEXT-f1 private L1 (Table III); 0 sets = none */
     uint32_t l1_miss_lat;        /* "L1 miss cycle" countdown, >= 1 */
-    uint32_t inject_mode;        /* 0: R7; 1: an ejecting flit frees its slot (NEXT-f4) */
+    uint32_t inject_mode;        /* 0: R7; 1: an ejecting flit frees its slot (NEXT-f4);
+                                    2: queued flits fill every free input slot (NEXT-f4, R53) */
     uint32_t age_base;           /* test knob: age of a newly injected flit (0 = P:L259) */
     uint32_t mig_hist;           /* NEXT-f2: accessor history length N; 0 = no migration */
     uint32_t nfl_b2;             /* NEXT-f2: flits of a B2 block migration (Table I: 16), 1..16 */
@@ -112,6 +113,11 @@ void orc_philox(uint32_t k0, uint32_t k1, const uint32_t c[4], uint32_t out[4]);
 int orc_arbitrate(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
                   uint32_t nf, const uint64_t *flits, int *out_port,
                   uint64_t *out_age);
+/* The same with stride 4 or 7 u64 per flit {dst, src, age, inj[, fid, kind,
+ * payload]}: the last three break ties of equal (age, inj, src) -- flits one
+ * node injected in the same cycle under the fill-all mode (R53). */
+int orc_arbitrate_ex(uint32_t mesh_w, uint32_t mesh_h, uint32_t node, uint32_t prio, uint32_t route,
+                     uint32_t nf, uint32_t stride, const uint64_t *flits, int *out_port, uint64_t *out_age);
 
 /* In-flight flits on links (inputs of the next cycle) and their age sum. */
 int64_t orc_links_occupied(const orc_sim *s, int64_t *age_sum);

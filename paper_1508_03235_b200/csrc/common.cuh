@@ -172,7 +172,7 @@ struct Dev {
     uint32_t mode, prio, route, sets, ways, tpn, priv, thr_inj, thr_priv, l2_hit_lat, mem_lat, nfl_ra;
     uint32_t dir_mode, dir_node;      // NEXT-f3: central directory at dir_node (R40)
     uint32_t l1_sets, l1_ways, l1_miss_lat;   // NEXT-f1 private L1 (R42); 0 sets = none
-    uint32_t inject_mode;             // NEXT-f4: an ejecting flit frees its slot (R43)
+    uint32_t inject_mode;             // NEXT-f4: 1 an ejecting flit frees its slot (R43), 2 fill all free slots (R53)
     uint32_t age_base;                // test knob: age of an injected flit (0 = P:L259)
     uint32_t mig_hist, nfl_b2;        // NEXT-f2: accessor history length (0 = off), B2 flits
     uint64_t loc_n;                   // directory entries held by this band

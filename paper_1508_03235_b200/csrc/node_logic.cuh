@@ -803,6 +803,15 @@ __device__ __forceinline__ uint64_t prio_key(const Dev &S, const Flit &f, uint32
     return k;
 }
 
+// Tie-break of equal priority keys (R53): only flits one node injected in the
+// same cycle (fill-all injection) share (age, inj, src); they rank by fid,
+// kind, dst, payload ascending -- a SMALLER secondary key ranks first.  Flits
+// equal in all of these are identical (either order gives the same state).
+__device__ __forceinline__ uint64_t sec_key(const Flit &f)
+{
+    return ((uint64_t)f_fid(f) << 56) | ((uint64_t)f_kind(f) << 53) | ((uint64_t)f_dst(f) << 32) | f.w;
+}
+
 // dst -> (x, y) without a hardware divide: umulhi by ceil(2^32/W) is exact for
 // node ids < 2^21 (W <= 2048)
 __device__ __forceinline__ uint32_t row_of(const Dev &S, uint32_t n) { return __umulhi(n, S.wmagic); }
@@ -888,7 +897,9 @@ __device__ __forceinline__ uint32_t route_select(const Dev &S, const NodeCtx &c,
         Flit f = in.f[0];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            if (((left >> k) & 1u) && key[k] > bk) { bk = key[k]; bi = k; f = in.f[k]; }
+            if (!((left >> k) & 1u)) continue;
+            const bool tie_first = S.inject_mode == 2u && key[k] == bk && sec_key(in.f[k]) < sec_key(f);
+            if (key[k] > bk || tie_first) { bk = key[k]; bi = k; f = in.f[k]; }
         }
         left &= ~(1u << bi);
         const uint32_t dst = f_dst(f);
@@ -1012,6 +1023,16 @@ __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t n
 
 __device__ __forceinline__ void inject(const Dev &S, NodeCtx &c, Inputs &in, uint64_t t, Acc &acc)
 {
+    if (S.inject_mode == 2u) {
+        // NEXT-f4 fill-all (R53): queued flits fill every
+        // free input slot, oldest-queued first (empty link slots, so the
+        // injection register stays unused; ranking ties: sec_key)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (!((in.present >> k) & 1u) && inject_flit(S, c, (uint32_t)__popc(in.present), t, acc, in.f[k]))
+                in.present |= 1u << k;
+        return;
+    }
     uint32_t frees = 0u;
     if (S.inject_mode)
 #pragma unroll

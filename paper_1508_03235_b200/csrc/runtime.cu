@@ -136,7 +136,7 @@ static int validate(const noc_sim_config *c)
     if (c->bands > MAX_BANDS || c->bands > c->mesh_h) return fail(NOC_EINVAL, "bands must be <= 8 and <= mesh_h");
     if (c->bands > 1 && c->world_size > 1) return fail(NOC_EINVAL, "bands > 1 is for world_size == 1 only");
     if (c->engine > NOC_ENGINE_TILED4) return fail(NOC_EINVAL, "unknown engine");
-    if (c->inject_mode > 1) return fail(NOC_EINVAL, "inject_mode out of range");
+    if (c->inject_mode > 2) return fail(NOC_EINVAL, "inject_mode out of range");
     if (c->age_base > AGE_MAX) return fail(NOC_EINVAL, "age_base > 65535 (R32)");
     if (c->band_streams > 1) return fail(NOC_EINVAL, "band_streams must be 0 or 1");
     if (c->mig_hist > 16) return fail(NOC_EINVAL, "mig_hist must be 0..16");
@@ -147,7 +147,7 @@ static int validate(const noc_sim_config *c)
                             (c->engine != NOC_ENGINE_TILED && c->engine != NOC_ENGINE_AUTO)))
         return fail(NOC_EINVAL, "band_streams needs bands >= 2 in one process and the TILED engine");
     if (c->inject_mode && c->engine == NOC_ENGINE_TILED4)
-        return fail(NOC_EINVAL, "inject_mode 1 needs five flit lanes per router: not with the TILED4 engine");
+        return fail(NOC_EINVAL, "inject_mode 1/2 (NEXT-f4) are not supported by the TILED4 engine");
     if (c->mode == NOC_MODE_LSPD && c->l1_sets &&
         (c->l1_sets > 65536 || c->l1_ways < 1 || c->l1_ways > 16 || c->l1_miss_lat < 1 || c->l1_miss_lat >= (1u << 29)))
         return fail(NOC_EINVAL, "l1 geometry: sets 0..65536, ways 1..16, miss latency 1..2^29-1");
@@ -453,7 +453,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         cudaError_t ce = cudaErrorInvalidConfiguration;
         if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
                           : tiled_prepare(cfg->mode == NOC_MODE_LSPD && cfg->l1_sets ? 2u : cfg->mode,
-                                          cfg->route | (cfg->inject_mode << 1) | (s->nb > 1 || s->world > 1 ? 4u : 0u),
+                                          cfg->route | (cfg->inject_mode ? 2u : 0u) | (s->nb > 1 || s->world > 1 ? 4u : 0u),
                                           cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {
             s->engine = cand;

@@ -171,7 +171,7 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
     const bool dr = activity != nullptr;
     const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr,
-                              P.d[0].route | (P.d[0].inject_mode << 1) | (P.general ? 4u : 0u));
+                              P.d[0].route | (P.d[0].inject_mode ? 2u : 0u) | (P.general ? 4u : 0u));
     // the dynamic shared-memory limit is a per-function (process-wide)
     // attribute: another handle of a different size may have lowered it
     {

@@ -578,11 +578,22 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             for (uint32_t d = 0; d < 5; ++d) f[d] = Flit{0, 0, 0, 0};
 #pragma unroll
             for (uint32_t d = 0; d < 4; ++d) lds128_if((present >> d) & 1u, fw + d * 16u * np, f[d]);
-            uint32_t frees = 0u;   // NEXT-f4 injection mode (R43): an ejecting flit frees its port
-            if (FEAT & 2u)
+            // NEXT-f4 (FEAT bit 1): injection mode 1 (R43), an ejecting flit
+            // frees its port; mode 2 (R53), queued flits fill every free input
+            // slot (the empty link slots; ranking ties: sec_key)
+            const bool fill_all = (FEAT & 2u) && S.inject_mode == 2u;
+            if (fill_all) {
 #pragma unroll
-                for (uint32_t d = 0; d < 4; ++d) frees |= ((present >> d) & 1u) && f_dst(f[d]) == c.n;
-            if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4], frees)) present |= 16u;
+                for (uint32_t d = 0; d < 4; ++d)
+                    if (!((present >> d) & 1u) && inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[d]))
+                        present |= 1u << d;
+            } else {
+                uint32_t frees = 0u;
+                if (FEAT & 2u)
+#pragma unroll
+                    for (uint32_t d = 0; d < 4; ++d) frees |= ((present >> d) & 1u) && f_dst(f[d]) == c.n;
+                if (inject_flit(S, c, (uint32_t)__popc(present), t, acc, f[4], frees)) present |= 16u;
+            }
             TRACE_EV(((present & 16u) ? 32u : 0u) | (present ? 64u : 0u) | (ext ? 128u : 0u));
 
             // (2) first choices (eject at the destination, else x-port, else
@@ -638,7 +649,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 for (uint32_t a = 0; a < 4; ++a)
 #pragma unroll
                     for (uint32_t b = a + 1; b < 4; ++b) {
-                        if (key[a] > key[b]) ++rk[b];
+                        // equal keys only under fill-all (flits one node injected
+                        // together): the smaller secondary key ranks first (R53)
+                        const bool first = (FEAT & 2u) && key[a] == key[b] && key[a] != 0ull
+                                               ? sec_key(f[a]) < sec_key(f[b]) : key[a] > key[b];
+                        if (first) ++rk[b];
                         else ++rk[a];
                     }
                 uint32_t ord = 4u << 16;

@@ -528,3 +528,33 @@ def test_migration_c3_and_bands():
         g.run(1500)
         o.run(1500)
         assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", [nb.ENGINE_STEP, nb.ENGINE_PERSIST, nb.ENGINE_TILED])
+@pytest.mark.parametrize("cfg", [
+    W.make(mesh_w=16, mesh_h=16, mode=W.MODE_UR, lam=0.4, inject_mode=2),
+    W.make(mesh_w=13, mesh_h=11, mode=W.MODE_UR, lam=0.2, inject_mode=2, prio=W.PRIO_OLDEST),
+    W.lspd(24, 20, lam=0.3, inject_mode=2, l1_sets=2, l1_ways=2),
+    W.c1b(inject_mode=2, route=W.ROUTE_XY),
+    W.lspd(20, 18, lam=0.2, inject_mode=2, mig_hist=6, nfl_b2=16, sendq_cap=64),
+], ids=["ur16_sat", "ur13x11_oldest", "lspd24x20_l1", "c1b_xy", "lspd20x18_mig"])
+def test_fill_all_injection_gpu(cfg, engine):
+    """NEXT-f4 fill-all injection (R53): several flits per node and cycle,
+    ranking ties broken by (fid, kind, dst, payload) -- bit-exact against the
+    oracle, with a drain."""
+    g, o = both(cfg, 3000, engine, drain=200000)
+    assert_same(g, o)
+
+
+def test_fill_all_c3_bands_and_tiled4_rejected():
+    g, o = both(W.c3(inject_mode=2), 800, split=[300, 499, 1])
+    assert_same(g, o)
+    cfg = W.lspd(40, 37, lam=0.3, inject_mode=2)
+    g = nb.NocSim(cfg, bands=3, engine=nb.ENGINE_TILED)
+    o = Oracle(cfg)
+    for k in (7, 400, 993):
+        g.run(k)
+        o.run(k)
+    assert_same(g, o)
+    with pytest.raises(nb.NocSimError):
+        nb.NocSim(W.c1b(inject_mode=2), engine=nb.ENGINE_TILED4)
