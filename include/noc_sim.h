@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define NOC_SIM_ABI_VERSION 5u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base; 4: band_streams; 5: migration */
+#define NOC_SIM_ABI_VERSION 6u   /* 2: route, dir_mode/dir_node, l1_*, inject_mode; L1 counters; 3: age_base; 4: band_streams; 5: migration; 6: memory nodes, hub FIFOs, fill-all injection */
 
 /* error codes */
 #define NOC_OK          0
@@ -53,6 +53,18 @@ extern "C" {
 #define NOC_DIR_DISTRIBUTED 0u /* home(T) = T mod N (R12)                          */
 #define NOC_DIR_CENTRAL     1u /* home(T) = dir_node for every T: the paper's
                                   centralized location array     */
+
+/* memory placement (DESIGN R54-R55) */
+#define NOC_MEM_OFFMESH 0u  /* off-mesh memory at the requester, fixed mem_lat (R17) */
+#define NOC_MEM_HOME    1u  /* memory at the block's home node: the directory node
+                               under NOC_DIR_CENTRAL; a negative
+                               directory reply becomes a B2 fill from there (P:L69,
+                               L89, Table I B2 = nfl_b2 flits)                 */
+#define NOC_MEM_CTRLS   2u  /* mem_ctrls memory-controller nodes, ceil(M/2) evenly
+                               spaced on the top row and the rest on the bottom
+                               row; block T's memory = controller T mod M: a
+                               1-flit request, a B2 fill back, B2 writebacks of
+                               every L2 victim                                 */
 
 /* routing (DESIGN R3, R5; SURVEY 8(f) NEXT-f4 compatibility mode) */
 #define NOC_ROUTE_PMDR   0u /* productive ports x then y; deflect to the first free
@@ -144,8 +156,19 @@ typedef struct noc_sim_config {
                                   history ("last N (say 10) accesses"),
                                   1..16; 0 = no migration (the base model).
                                   Needs tags_per_node*N <= 2^28              */
-    uint32_t nfl_b2;           /* flits of a B2 block migration (Table I: 16),
-                                  1..16 (ignored when mig_hist = 0)          */
+    uint32_t nfl_b2;           /* flits of a B2 block (Table I: 16), 1..16: a
+                                  block migration (mig_hist > 0) and the memory
+                                  fills / writebacks of mem_mode 1 and 2      */
+    uint32_t mem_mode;         /* LSPD, where memory is (DESIGN R54-R55):
+                                  NOC_MEM_OFFMESH, NOC_MEM_HOME, NOC_MEM_CTRLS.
+                                  1 and 2 exclude migration (mig_hist = 0)    */
+    uint32_t mem_ctrls;        /* NOC_MEM_CTRLS: number of controllers M,
+                                  1..64, ceil(M/2) <= mesh_w (ignored otherwise) */
+    uint32_t hub_sendq_cap;    /* send-FIFO packets at hub nodes -- the central
+                                  directory node (NOC_DIR_CENTRAL) and the
+                                  memory controllers (NOC_MEM_CTRLS); 0 =
+                                  sendq_cap, else a power of two in
+                                  sendq_cap..1024 (DESIGN R56)     */
 } noc_sim_config;
 
 /* Counters (DESIGN 3.6; Table II columns P:L303-304 and the statistics list
@@ -164,6 +187,9 @@ typedef struct noc_sim_counters {
      * updates, source invalidations, redirections sent / received */
     int64_t mig_requests, mig_nacks, migrations, mig_installs;
     int64_t dir_updates, invalidations, redirections, rr_received;
+    /* memory nodes (R55): B2 fills sent by memory nodes / completed at the
+     * requesters, B2 writebacks sent, writeback flits absorbed at memory nodes */
+    int64_t mem_fills_sent, mem_fills_received, mem_wbs_sent, mem_wb_flits;
 } noc_sim_counters;
 
 /* Runtime facts about a handle (for measurement and the bench). */

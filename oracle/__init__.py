@@ -31,6 +31,7 @@ KIND_NAMES = ("probe", "da", "dr", "ndr", "rq", "ra", "trap", "ev")
 L1_COUNTER_NAMES = ("l1_hits", "l1_misses", "wb_sent", "wb_received")   # NEXT-f1 (R42)
 MIG_COUNTER_NAMES = ("mig_requests", "mig_nacks", "migrations", "mig_installs",
                      "dir_updates", "invalidations", "redirections", "rr_received")   # NEXT-f2
+MEM_COUNTER_NAMES = ("mem_fills_sent", "mem_fills_received", "mem_wbs_sent", "mem_wb_flits")   # memory nodes (R55)
 
 MODE_UR, MODE_LSPD = 0, 1
 PRIO_DEFLECT, PRIO_OLDEST = 0, 1
@@ -64,12 +65,13 @@ class _Config(C.Structure):
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
         ("inject_mode", C.c_uint32), ("age_base", C.c_uint32),
         ("mig_hist", C.c_uint32), ("nfl_b2", C.c_uint32),
+        ("mem_mode", C.c_uint32), ("mem_ctrls", C.c_uint32), ("hub_sendq_cap", C.c_uint32),
     ]
 
 
 class _Counters(C.Structure):
     _fields_ = [("cycle", C.c_int64)] + [(n, C.c_int64) for n in COUNTER_NAMES] + [
-        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES]
+        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES + MEM_COUNTER_NAMES]
 
 
 _lib = None
@@ -219,7 +221,7 @@ class Oracle:
             d[n] = getattr(cnt, n)
         for i, k in enumerate(KIND_NAMES):
             d["drops_" + k] = cnt.drops[i]
-        for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES:
+        for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES + MEM_COUNTER_NAMES:
             d[n] = getattr(cnt, n)
         return d, list(hl), list(hd), list(ha)
 

@@ -32,7 +32,11 @@ enum { K_PROBE = 0, K_DA = 1, K_DR = 2, K_NDR = 3, K_RQ = 4, K_RA = 5, K_TRAP = 
 enum { SUB_MR = 1, SUB_MG = 2, SUB_MN = 3, SUB_MIG = 4, SUB_DU = 5, SUB_INV = 6, SUB_RR = 7 };
 #define CTL(sub, v) (((uint32_t)(sub) << 28) | (v))
 /* core modes ("miss under a miss is not allowed"; DESIGN 3.4) */
-enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4, M_L1WAIT = 5 };
+enum { M_IDLE = 0, M_L2WAIT = 1, M_WAIT_DIR = 2, M_WAIT_DATA = 3, M_MEMWAIT = 4, M_L1WAIT = 5,
+       M_MEMFETCH = 6 /* memory nodes (R55): waiting for a B2 fill from the memory node */ };
+/* memory nodes (R55): a memory request is a DA flit, a fill flit an RA flit,
+ * a writeback flit a TRAP flit, each with this payload bit (tags < 2^31) */
+#define MEM_BIT 0x80000000u
 
 #define HOLDER_NONE 0xFFFFFFFFu
 #define AGE_MAX     65535u   /* R32: field width of the deflection age */
@@ -80,6 +84,7 @@ typedef struct {
     int has_ej;        /* Router.XToProc: the flit ejected this cycle          */
     Flit ej;
     Packet *fifo;      /* Core.ToBeSend as a FIFO of packets (R21)             */
+    uint32_t cap;      /* its capacity (hub nodes may have more, R56)          */
     uint32_t head, count, next;   /* next = NextFlitAddress          */
     int mode;          /* Core.Wait, refined (DESIGN 3.4)                      */
     uint64_t ready, start;
@@ -215,14 +220,14 @@ static void enq(orc_sim *s, uint32_t n, uint32_t kind, uint32_t dst, uint32_t pa
 {
     Node *c = &s->nodes[n];
     if (dst == n) fail(s, ORC_EASSERT, "packet addressed to its own node");
-    if (c->count == s->cfg.sendq_cap) {
+    if (c->count == c->cap) {
         s->c.drops[kind] += 1;
         /* R21: an LSPD protocol message that is dropped leaves its requester
          * (or a directory entry) waiting for ever: the run is invalid */
         if (s->cfg.mode == ORC_MODE_LSPD) fail(s, ORC_EOVERFLOW, "send FIFO overflow in LSPD mode (R21)");
         return;
     }
-    Packet *p = &c->fifo[(c->head + c->count) % s->cfg.sendq_cap];
+    Packet *p = &c->fifo[(c->head + c->count) % c->cap];
     p->kind = kind; p->dst = dst; p->payload = payload; p->nfl = nfl;
     c->count += 1;
     s->c.packets_enqueued += 1;
@@ -274,6 +279,34 @@ static int l2_hit(orc_sim *s, uint32_t n, uint32_t T, uint32_t who)
 static uint32_t home_of(const orc_sim *s, uint32_t T)
 {
     return s->cfg.dir_mode ? s->cfg.dir_node : T % s->N;
+}
+
+/* Memory-controller node k of M (mem_mode 2, R54): ceil(M/2) controllers
+ * evenly spaced on the top row, the others on the bottom row */
+static uint32_t mem_ctrl_node(const orc_sim *s, uint32_t k)
+{
+    uint32_t M = s->cfg.mem_ctrls, Mt = (M + 1) / 2, Mb = M - Mt;
+    if (k < Mt) return (uint32_t)(((2ull * k + 1) * s->W) / (2ull * Mt));
+    uint32_t j = k - Mt;
+    return (s->H - 1) * s->W + (uint32_t)(((2ull * j + 1) * s->W) / (2ull * Mb));
+}
+
+/* The node holding block T's memory (R54) */
+static uint32_t mem_node(const orc_sim *s, uint32_t T)
+{
+    return s->cfg.mem_mode == 1 ? home_of(s, T) : mem_ctrl_node(s, T % s->cfg.mem_ctrls);
+}
+
+/* A B2 block (Table I: 16 flits) of the given kind and payload from n to dst,
+ * as packets of <= 8 flits (the send FIFO entry and fid hold 8, R50) */
+static void send_b2(orc_sim *s, uint32_t n, uint32_t dst, uint32_t kind, uint32_t payload)
+{
+    uint32_t left = s->cfg.nfl_b2;
+    while (left) {
+        uint32_t k = left > 8 ? 8 : left;
+        enq(s, n, kind, dst, payload, k);
+        left -= k;
+    }
 }
 
 /* EV handler at home h (R13): the only writer of loc[T] besides DIRSERVICE */
@@ -329,6 +362,13 @@ static void install(orc_sim *s, uint32_t n, uint32_t T)
             s->c.evs_sent += 1;
             if (hv == n) ev_handler(s, n, V, n);
             else enq(s, n, K_EV, hv, V, 1);
+        }
+        /* memory nodes (R55): "The evicted block need to be written back to
+         * the memory" -- a B2 block (Table I "L2 Blk Replacement",
+         * 16 flits) to V's memory node, absorbed there; none if it is here */
+        if (s->cfg.mem_mode && mem_node(s, V) != n) {
+            s->c.mem_wbs_sent += 1;
+            send_b2(s, n, mem_node(s, V), K_TRAP, V | MEM_BIT);
         }
     }
     L[victim].valid = 1;
@@ -399,14 +439,30 @@ static void complete(orc_sim *s, uint32_t n)
  * ("new request to next higher level memory"; P:L75 local placement). */
 #define NDR_NOINSTALL 0x80000000u   /* NEXT-f2 (R47): fetch without installing */
 #define NDR_PEND      0x40000000u   /* NEXT-f2 (R47): the reply counted an EV of the requester in flight */
+/* A memory access of the requester n (install: R14 / R16 / R47): off-mesh at
+ * the requester (R17), or -- memory nodes (R55) -- a 1-flit memory request
+ * to the block's memory node, whose B2 fill is followed by the memory latency
+ * at the requester; a memory node that is n itself serves it locally */
+static void mem_fetch(orc_sim *s, uint32_t n, int install)
+{
+    Node *c = &s->nodes[n];
+    s->c.mem_requests += 1;
+    c->install = install;
+    if (s->cfg.mem_mode && mem_node(s, c->tag) != n) {
+        enq(s, n, K_DA, mem_node(s, c->tag), c->tag | MEM_BIT, 1);
+        c->mode = M_MEMFETCH;
+        c->rx = 0;
+        return;
+    }
+    c->mode = M_MEMWAIT;
+    c->ready = s->t + s->cfg.mem_lat;
+}
+
 static void receive_ndr(orc_sim *s, uint32_t n, uint32_t payload)
 {
     Node *c = &s->nodes[n];
     if (c->mode != M_WAIT_DIR) fail(s, ORC_EASSERT, "NDR at a core that is not waiting for the directory");
-    s->c.mem_requests += 1;
-    c->mode = M_MEMWAIT;
-    c->install = (payload & NDR_NOINSTALL) ? 0 : (payload & NDR_PEND) ? 2 : 1;
-    c->ready = s->t + s->cfg.mem_lat;
+    mem_fetch(s, n, (payload & NDR_NOINSTALL) ? 0 : (payload & NDR_PEND) ? 2 : 1);
 }
 
 /* Positive directory reply: request the holder (Fig. 4 step 3) */
@@ -442,6 +498,12 @@ static void dir_service(orc_sim *s, uint32_t h, uint32_t T, uint32_t r)
     if (r == h) {                          /* loopback: no flits (R28) */
         if (kind == K_NDR) receive_ndr(s, r, payload);
         else receive_dr(s, r, payload);
+    } else if (kind == K_NDR && s->cfg.mem_mode == 1) {
+        /* memory at the directory (R55): "negative-DR -> memory
+         * fetch is a local handoff at that node followed by a ... reply to the
+         * requester": the home sends the B2 fill instead of the NDR */
+        s->c.mem_fills_sent += 1;
+        send_b2(s, h, r, K_RA, T | MEM_BIT);
     } else {
         enq(s, h, kind, r, payload, 1);
     }
@@ -933,7 +995,7 @@ static void phase2(orc_sim *s, uint32_t n)
         s->c.injected += 1;
         c->next += 1;
         if (c->next == p->nfl) {
-            c->head = (c->head + 1) % s->cfg.sendq_cap;
+            c->head = (c->head + 1) % c->cap;
             c->count -= 1;
             c->next = 0;
         }
@@ -1006,7 +1068,12 @@ static void phase3(orc_sim *s, uint32_t n)
         else s->c.probes_delivered += 1;
         break;
     case K_DA:
-        dir_service(s, n, f.payload, f.src);
+        if (f.payload & MEM_BIT) {                /* memory request at a memory node (R55) */
+            s->c.mem_fills_sent += 1;
+            send_b2(s, n, f.src, K_RA, f.payload);
+        } else {
+            dir_service(s, n, f.payload, f.src);
+        }
         break;
     case K_DR:
         receive_dr(s, n, f.payload);
@@ -1018,6 +1085,22 @@ static void phase3(orc_sim *s, uint32_t n)
         serve_rq(s, n, f.payload, f.src);
         break;
     case K_RA:
+        if (f.payload & MEM_BIT) {                /* a flit of a B2 memory fill (R55) */
+            if (c->mode != M_MEMFETCH && c->mode != M_WAIT_DIR) fail(s, ORC_EASSERT, "fill flit at a core not fetching");
+            if ((f.payload & ~MEM_BIT) != c->tag) fail(s, ORC_EASSERT, "fill flit of another block");
+            c->rx += 1;
+            if (c->rx == s->cfg.nfl_b2) {
+                c->rx = 0;
+                s->c.mem_fills_received += 1;
+                if (c->mode == M_WAIT_DIR) {      /* the home's memory answered the DA (mem_mode 1) */
+                    s->c.mem_requests += 1;
+                    c->install = 1;
+                }
+                c->mode = M_MEMWAIT;
+                c->ready = s->t + s->cfg.mem_lat;
+            }
+            break;
+        }
         if (c->mode != M_WAIT_DATA) fail(s, ORC_EASSERT, "RA flit at a core not waiting for data");
         c->rx += 1;
         if (c->rx == s->cfg.nfl_ra) {
@@ -1028,12 +1111,13 @@ static void phase3(orc_sim *s, uint32_t n)
         }
         break;
     case K_TRAP:
+        if (f.payload & MEM_BIT) {                /* a writeback flit at a memory node: absorbed (R55) */
+            s->c.mem_wb_flits += 1;
+            break;
+        }
         if (c->mode != M_WAIT_DATA) fail(s, ORC_EASSERT, "TRAP at a core not waiting for data");
         s->c.traps_received += 1;
-        s->c.mem_requests += 1;
-        c->mode = M_MEMWAIT;
-        c->install = 0;                           /* R16: no install */
-        c->ready = s->t + s->cfg.mem_lat;
+        mem_fetch(s, n, 0);                       /* R16: no install */
         break;
     case K_EV:
         if (f.payload & WB_BIT) s->c.wb_received += 1;   /* L1 writeback: absorbed (R42) */
@@ -1149,6 +1233,18 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         return ORC_EINVAL;
     }
     if (cfg->nfl_ra < 1 || cfg->nfl_ra > 8) { set_err("nfl_ra must be 1..8"); return ORC_EINVAL; }
+    if (cfg->mem_mode > 2 || (cfg->mem_mode && (cfg->mode != ORC_MODE_LSPD || cfg->mig_hist ||
+                                                cfg->nfl_b2 < 1 || cfg->nfl_b2 > 16))) {
+        set_err("memory nodes (mem_mode 1/2) need LSPD mode, no migration and nfl_b2 1..16 (R54)");
+        return ORC_EINVAL;
+    }
+    if (cfg->mem_mode == 2 && (cfg->mem_ctrls < 1 || cfg->mem_ctrls > 64 || (cfg->mem_ctrls + 1) / 2 > W)) {
+        set_err("mem_ctrls must be 1..64 with ceil(M/2) <= mesh_w"); return ORC_EINVAL;
+    }
+    if (cfg->hub_sendq_cap && (cfg->hub_sendq_cap < cfg->sendq_cap || cfg->hub_sendq_cap > 1024 ||
+                               (cfg->hub_sendq_cap & (cfg->hub_sendq_cap - 1)))) {
+        set_err("hub_sendq_cap must be 0 or a power of two in sendq_cap..1024"); return ORC_EINVAL;
+    }
     uint64_t N = (uint64_t)W * H;
     if (cfg->mode == ORC_MODE_LSPD) {
         if (cfg->l2_sets < 1 || cfg->l2_sets > 65536 || cfg->l2_ways < 1 || cfg->l2_ways > 16) {
@@ -1179,7 +1275,9 @@ int orc_create(const orc_config *cfg, orc_sim **out)
     s->W = W; s->H = H; s->N = (uint32_t)N;
     s->gen_enabled = 1;
     s->nodes = calloc(N, sizeof(Node));
-    s->fifo_store = calloc(N * cfg->sendq_cap, sizeof(Packet));
+    /* hub nodes (R56): the central directory node and the memory controllers */
+    const uint32_t hub_cap = cfg->hub_sendq_cap ? cfg->hub_sendq_cap : cfg->sendq_cap;
+    s->fifo_store = calloc(N * cfg->sendq_cap + (uint64_t)65 * hub_cap, sizeof(Packet));
     s->hl = calloc(cfg->hist_bins, sizeof(uint64_t));
     s->hd = calloc(cfg->hist_bins, sizeof(uint64_t));
     s->ha = calloc(cfg->hist_bins, sizeof(uint64_t));
@@ -1220,7 +1318,22 @@ int orc_create(const orc_config *cfg, orc_sim **out)
     if (bad) { orc_destroy(s); set_err("out of memory"); return ORC_ENOMEM; }
     for (uint64_t n = 0; n < N; ++n) {
         s->nodes[n].fifo = &s->fifo_store[n * cfg->sendq_cap];
+        s->nodes[n].cap = cfg->sendq_cap;
         s->nodes[n].mode = M_IDLE;
+    }
+    {
+        Packet *next = &s->fifo_store[N * cfg->sendq_cap];   /* hub FIFOs after the ordinary ones */
+        uint32_t hubs[65], nh = 0;
+        if (cfg->dir_mode == 1) hubs[nh++] = cfg->dir_node;
+        if (cfg->mem_mode == 2)
+            for (uint32_t k = 0; k < cfg->mem_ctrls; ++k) hubs[nh++] = mem_ctrl_node(s, k);
+        for (uint32_t i = 0; i < nh; ++i) {
+            Node *c = &s->nodes[hubs[i]];
+            if (c->fifo >= &s->fifo_store[N * cfg->sendq_cap]) continue;   /* listed twice */
+            c->fifo = next;
+            c->cap = hub_cap;
+            next += hub_cap;
+        }
     }
     {
         uint64_t i = 0;
@@ -1329,7 +1442,7 @@ uint64_t orc_state_hash(const orc_sim *s)
             H += term(D_LINK, (uint64_t)n * 4 + d, v, 7);
         }
         for (uint32_t k = 0; k < c->count; ++k) {
-            const Packet *p = &c->fifo[(c->head + k) % s->cfg.sendq_cap];
+            const Packet *p = &c->fifo[(c->head + k) % c->cap];
             v[0] = p->kind; v[1] = p->dst; v[2] = p->payload; v[3] = p->nfl;
             H += term(D_FIFO, ((uint64_t)n << 16) + k, v, 4);
         }
@@ -1342,6 +1455,7 @@ uint64_t orc_state_hash(const orc_sim *s)
             case M_WAIT_DATA: tag = c->tag; rx = c->rx; break;
             case M_MEMWAIT:   ready = c->ready; tag = c->tag; inst = (uint64_t)c->install; break;
             case M_L1WAIT:    ready = c->ready; tag = c->tag; break;
+            case M_MEMFETCH:  tag = c->tag; inst = (uint64_t)c->install; rx = c->rx; break;
             }
             v[0] = (uint64_t)c->mode; v[1] = ready; v[2] = tag; v[3] = inst; v[4] = start; v[5] = rx;
             H += term(D_CORE, n, v, 6);
@@ -1507,7 +1621,7 @@ int orc_fifo(const orc_sim *s, uint32_t n, uint32_t k, uint64_t out[2], uint64_t
     const Node *c = &s->nodes[n];
     out[0] = c->count; out[1] = c->next;
     if (k < c->count) {
-        const Packet *p = &c->fifo[(c->head + k) % s->cfg.sendq_cap];
+        const Packet *p = &c->fifo[(c->head + k) % c->cap];
         pkt[0] = p->kind; pkt[1] = p->dst; pkt[2] = p->payload; pkt[3] = p->nfl;
     }
     return ORC_OK;
@@ -1561,7 +1675,7 @@ int orc_poke(orc_sim *s, uint32_t field, uint32_t n, uint32_t i, uint32_t j, uin
     case 5: if (n >= s->ntags) return ORC_EINVAL; s->loc[n].pend += (uint32_t)value; return ORC_OK;
     case 6:
         if (!c || i >= c->count) return ORC_EINVAL;
-        c->fifo[(c->head + i) % s->cfg.sendq_cap].payload ^= (uint32_t)value; return ORC_OK;
+        c->fifo[(c->head + i) % c->cap].payload ^= (uint32_t)value; return ORC_OK;
     case 7: if (!c) return ORC_EINVAL; c->next = (uint32_t)value; return ORC_OK;
     case 8: {
         int ncnt = (int)((sizeof(orc_counters) - sizeof(int64_t)) / sizeof(int64_t));

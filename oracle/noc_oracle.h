@@ -72,7 +72,16 @@ typedef struct {
                                     2: queued flits fill every free input slot (NEXT-f4, R53) */
     uint32_t age_base;           /* test knob: age of a newly injected flit (0 = P:L259) */
     uint32_t mig_hist;           /* NEXT-f2: accessor history length N; 0 = no migration */
-    uint32_t nfl_b2;             /* NEXT-f2: flits of a B2 block migration (Table I: 16), 1..16 */
+    uint32_t nfl_b2;             /* flits of a B2 block (Table I: 16), 1..16: migration (NEXT-f2)
+                                    and memory fills / writebacks (mem_mode >= 1) */
+    uint32_t mem_mode;           /* memory placement (R54): 0 off-mesh at the requester (R17);
+                                    1 at the home node of the block (the directory node under
+                                    the central directory); 2 mem_ctrls
+                                    memory-controller nodes on the top / bottom rows (NEXT-f4) */
+    uint32_t mem_ctrls;          /* mem_mode 2: number of controllers M, 1..64, ceil(M/2) <= W */
+    uint32_t hub_sendq_cap;      /* send-FIFO packets at hub nodes (the central directory node,
+                                    the memory controllers; R56): 0 = sendq_cap, else a power
+                                    of two in sendq_cap..1024 */
 } orc_config;
 
 /* counters, in the order of DESIGN.md section 3.6 */
@@ -87,6 +96,10 @@ typedef struct {
     int64_t l1_hits, l1_misses, wb_sent, wb_received;   /* NEXT-f1 (R42) */
     int64_t mig_requests, mig_nacks, migrations, mig_installs;   /* NEXT-f2 (R44-R52) */
     int64_t dir_updates, invalidations, redirections, rr_received;
+    /* memory nodes (mem_mode >= 1, R54-R55): B2 fills sent by memory nodes
+     * and completed at requesters, B2 writebacks sent, writeback flits
+     * absorbed by memory nodes */
+    int64_t mem_fills_sent, mem_fills_received, mem_wbs_sent, mem_wb_flits;
 } orc_counters;
 
 typedef struct orc_sim orc_sim;

@@ -29,6 +29,7 @@ KIND_NAMES = ("probe", "da", "dr", "ndr", "rq", "ra", "trap", "ev")
 L1_COUNTER_NAMES = ("l1_hits", "l1_misses", "wb_sent", "wb_received")   # NEXT-f1 (R42)
 MIG_COUNTER_NAMES = ("mig_requests", "mig_nacks", "migrations", "mig_installs",
                      "dir_updates", "invalidations", "redirections", "rr_received")   # NEXT-f2
+MEM_COUNTER_NAMES = ("mem_fills_sent", "mem_fills_received", "mem_wbs_sent", "mem_wb_flits")   # memory nodes (R55)
 
 NOC_OK, NOC_EINVAL, NOC_ENOMEM, NOC_ECUDA, NOC_ENCCL, NOC_EOVERFLOW, NOC_ESTATE = 0, -1, -2, -3, -4, -5, -6
 ENGINE_AUTO, ENGINE_STEP, ENGINE_PERSIST, ENGINE_TILED, ENGINE_TILED4 = 0, 1, 2, 3, 4
@@ -53,12 +54,13 @@ class noc_sim_config(C.Structure):
         ("l1_sets", C.c_uint32), ("l1_ways", C.c_uint32), ("l1_miss_lat", C.c_uint32),
         ("inject_mode", C.c_uint32), ("age_base", C.c_uint32), ("band_streams", C.c_uint32),
         ("mig_hist", C.c_uint32), ("nfl_b2", C.c_uint32),
+        ("mem_mode", C.c_uint32), ("mem_ctrls", C.c_uint32), ("hub_sendq_cap", C.c_uint32),
     ]
 
 
 class noc_sim_counters(C.Structure):
     _fields_ = [("cycle", C.c_int64)] + [(n, C.c_int64) for n in COUNTER_NAMES] + [
-        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES]
+        ("drops", C.c_int64 * 8)] + [(n, C.c_int64) for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES + MEM_COUNTER_NAMES]
 
 
 class noc_sim_info(C.Structure):
@@ -99,7 +101,7 @@ def lib():
         L.noc_sim_destroy.argtypes = [P]
         L.noc_sim_last_error.restype = C.c_char_p
         L.noc_sim_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
-        if L.noc_sim_abi_version() != 5:   # include/noc_sim.h NOC_SIM_ABI_VERSION
+        if L.noc_sim_abi_version() != 6:   # include/noc_sim.h NOC_SIM_ABI_VERSION
             raise NocSimError(NOC_EINVAL, "ABI version mismatch")
         _lib = L
     return _lib
@@ -167,7 +169,7 @@ def noc_sim_stats(h, nbins: int):
         d[n] = getattr(cnt, n)
     for i, k in enumerate(KIND_NAMES):
         d["drops_" + k] = cnt.drops[i]
-    for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES:
+    for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES + MEM_COUNTER_NAMES:
         d[n] = getattr(cnt, n)
     return d, list(hl), list(hd), list(ha)
 

@@ -13,7 +13,11 @@ enum : uint32_t { PN = 0, PS = 1, PE = 2, PW = 3, PX = 4 };
 // message kinds (Table I; DESIGN 3.2)
 enum : uint32_t { KPROBE = 0, KDA = 1, KDR = 2, KNDR = 3, KRQ = 4, KRA = 5, KTRAP = 6, KEV = 7 };
 // core modes (DESIGN 3.2)
-enum : uint32_t { MIDLE = 0, ML2WAIT = 1, MWAITDIR = 2, MWAITDATA = 3, MMEMWAIT = 4, ML1WAIT = 5 };
+enum : uint32_t { MIDLE = 0, ML2WAIT = 1, MWAITDIR = 2, MWAITDATA = 3, MMEMWAIT = 4, ML1WAIT = 5,
+                  MMEMFETCH = 6 /* memory nodes (R55): waiting for a B2 fill */ };
+// memory nodes (R55): a memory request is a DA flit, a memory fill flit an RA
+// flit, a memory writeback flit a TRAP flit, each with this payload bit
+constexpr uint32_t MEM_BIT = 0x80000000u;
 // an EV flit whose payload carries this bit is an L1 victim writeback (NEXT-f1, R42;
 // tags are < 2^31, R32)
 constexpr uint32_t WB_BIT = 0x80000000u;
@@ -24,7 +28,9 @@ enum : uint32_t {
     C_TRAPSENT, C_TRAPRCVD, C_MEMREQ, C_INSTALLS, C_EVICTIONS, C_EVSENT, C_EVRCVD,
     C_DROPS = 23, C_L1HIT = 31, C_L1MISS, C_WBSENT, C_WBRCVD,
     // NEXT-f2 migration + redirection (R44-R52)
-    C_MIGREQ = 35, C_MIGNACK, C_MIGS, C_MIGINST, C_DIRUPD, C_INVAL, C_REDIR, C_RRRCVD, NCOUNTERS = 43
+    C_MIGREQ = 35, C_MIGNACK, C_MIGS, C_MIGINST, C_DIRUPD, C_INVAL, C_REDIR, C_RRRCVD,
+    // memory nodes (R54-R55)
+    C_MEMFILLSENT = 43, C_MEMFILLRCVD, C_MEMWBSENT, C_MEMWBFLITS, NCOUNTERS = 47
 };
 // NEXT-f2 (R50): migration / redirection messages use the PROBE kind code in
 // LSPD mode, the message in payload bits 28-30, a tag or node id in bits 0-27
@@ -47,6 +53,16 @@ __host__ __device__ __forceinline__ uint32_t lw_make(uint32_t st, uint32_t cnt, 
 }
 // a line holds a block iff tag+1 != 0 and it is not a forwarding ghost
 __host__ __device__ __forceinline__ bool line_valid(const uint4 &v) { return v.x != 0u && lw_state(v.w) != MS_FWD; }
+// Memory-controller node k of M (mem_mode 2, R54): ceil(M/2) controllers
+// evenly spaced on the top row, the others on the bottom row
+__host__ __device__ __forceinline__ uint32_t mem_ctrl_node(uint32_t W, uint32_t H, uint32_t M, uint32_t k)
+{
+    const uint32_t Mt = (M + 1u) / 2u, Mb = M - Mt;
+    if (k < Mt) return (uint32_t)(((2ull * k + 1ull) * W) / (2ull * Mt));
+    const uint32_t j = k - Mt;
+    return (H - 1u) * W + (uint32_t)(((2ull * j + 1ull) * W) / (2ull * Mb));
+}
+
 // error flags
 enum : uint32_t { ERR_AGE = 1, ERR_PEND = 2, ERR_EVHOLDER = 4, ERR_PROTO = 8, ERR_DROP = 16, ERR_MIGRX = 32 };
 
@@ -175,6 +191,8 @@ struct Dev {
     uint32_t inject_mode;             // NEXT-f4: 1 an ejecting flit frees its slot (R43), 2 fill all free slots (R53)
     uint32_t age_base;                // test knob: age of an injected flit (0 = P:L259)
     uint32_t mig_hist, nfl_b2;        // NEXT-f2: accessor history length (0 = off), B2 flits
+    uint32_t mem_mode, mem_ctrls;     // memory placement (R54): 0 off-mesh, 1 home node, 2 controllers
+    uint32_t hub_cap;                 // send-FIFO capacity of hub nodes (R56)
     uint64_t loc_n;                   // directory entries held by this band
     uint32_t qcap, nb, seed_lo, seed_hi;
     uint32_t wmagic;                  // ceil(2^32 / W): row of a node id by umulhi
@@ -187,6 +205,8 @@ struct Dev {
     uint4 *core_cold;                 // [nloc]
     uint32_t *fifo_ctl;               // [nloc]
     uint2 *fifo_pkt;                  // [nloc][qcap]
+    uint8_t *hub_of;                  // [nloc] 0, or 1 + index of the node's hub FIFO in hub_pkt (R56); null = no hubs
+    uint2 *hub_pkt;                   // [hubs in this band][hub_cap]
     uint4 *l2;                        // [nloc][sets][ways] {tag+1 (0 = invalid), stamp_lo, stamp_hi, 0}
     uint4 *l1;                        // [nloc][l1_sets][l1_ways] {tag+1, stamp_lo, stamp_hi, owner} (NEXT-f1)
     uint32_t *loc;                    // [tpn][nloc] directory entries of tags homed in this band

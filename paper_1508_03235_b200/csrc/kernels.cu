@@ -237,7 +237,8 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
         }
         uint32_t q = S.fifo_ctl[l];
         for (uint32_t k = 0; k < q_count(q); ++k) {
-            uint2 p = S.fifo_pkt[(size_t)l * S.qcap + ((q_head(q) + k) & (S.qcap - 1u))];
+            const FifoRef F = fifo_of(S, l);
+            uint2 p = F.p[(q_head(q) + k) & (F.cap - 1u)];
             TupleHash th(4);
             th.add((p.x >> 21) & 7u).add(p.x & NODE_MASK).add(p.y).add((p.x >> 24) & 15u);
             H += hterm(D_FIFO, (n << 16) + k, th.h);
@@ -256,6 +257,7 @@ __global__ void k_hash_nodes(Dev S, uint64_t t, unsigned long long *out)
                 case ML1WAIT: ready = r29; tag = cold.z; break;
                 case MWAITDIR: tag = cold.z; break;
                 case MWAITDATA: tag = cold.z; rx = cold.w >> 2; break;
+                case MMEMFETCH: tag = cold.z; inst = cold.w & 3u; rx = cold.w >> 2; break;
                 default: ready = r29; tag = cold.z; inst = cold.w & 3u; break;
                 }
                 TupleHash th(6);

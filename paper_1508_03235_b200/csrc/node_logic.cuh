@@ -68,21 +68,38 @@ __device__ __forceinline__ void set_mode(NodeCtx &c, uint32_t mode, uint64_t rea
     c.hot_dirty = true;
 }
 
+// Send-FIFO storage of local node l: its packet ring and capacity.  Hub nodes
+// (the central directory node, the memory controllers) may have a larger one
+// (R56); only the rare FIFO paths (enqueue, head refill) look this up.
+struct FifoRef {
+    uint2 *p;
+    uint32_t cap;
+};
+__device__ __forceinline__ FifoRef fifo_of(const Dev &S, uint32_t l)
+{
+    if (S.hub_of) {
+        const uint32_t h = S.hub_of[l];
+        if (h) return FifoRef{S.hub_pkt + (size_t)(h - 1u) * S.hub_cap, S.hub_cap};
+    }
+    return FifoRef{S.fifo_pkt + (size_t)l * S.qcap, S.qcap};
+}
+
 // ENQ (DESIGN 3.3; bounded send FIFO, R21)
 __device__ __forceinline__ void enq(const Dev &S, const Sink &K, NodeCtx &c, uint32_t kind, uint32_t dst,
                                     uint32_t payload, uint32_t nfl)
 {
     uint32_t h = q_head(c.qctl), cnt = q_count(c.qctl);
-    if (cnt == S.qcap) {
+    const FifoRef F = fifo_of(S, c.l);
+    if (cnt == F.cap) {
         K.cnt(S, C_DROPS + kind);
         // R21: in LSPD mode a dropped protocol message would leave a core or a
         // directory entry waiting for ever, so the run is invalid: poison it
         if (S.mode != 0u) atomicOr(S.err, ERR_DROP);
         return;
     }
-    uint32_t slot = (h + cnt) & (S.qcap - 1u);
+    uint32_t slot = (h + cnt) & (F.cap - 1u);
     const uint2 pkt = make_uint2(dst | (kind << 21) | (nfl << 24), payload);
-    S.fifo_pkt[(size_t)c.l * S.qcap + slot] = pkt;
+    F.p[slot] = pkt;
     if (cnt == 0u) { c.head = pkt; c.head_ok = true; }
     c.qctl = q_make(h, cnt + 1u, q_next(c.qctl));
     c.q_dirty = true;
@@ -94,6 +111,24 @@ __device__ __forceinline__ void enq(const Dev &S, const Sink &K, NodeCtx &c, uin
 __device__ __forceinline__ uint32_t home_of(const Dev &S, uint32_t T)
 {
     return S.dir_mode ? S.dir_node : T % S.N;
+}
+
+// The node holding block T's memory (R54): its home, or its controller
+__device__ __forceinline__ uint32_t mem_node(const Dev &S, uint32_t T)
+{
+    return S.mem_mode == 1u ? home_of(S, T) : mem_ctrl_node(S.W, S.H, S.mem_ctrls, T % S.mem_ctrls);
+}
+
+// A B2 block (Table I: nfl_b2 flits) of the given kind and payload to dst, as
+// packets of <= 8 flits (R50)
+__device__ __forceinline__ void send_b2(const Dev &S, const Sink &K, NodeCtx &c, uint32_t dst, uint32_t kind,
+                                        uint32_t payload)
+{
+    for (uint32_t left = S.nfl_b2; left;) {
+        const uint32_t k = left > 8u ? 8u : left;
+        enq(S, K, c, kind, dst, payload, k);
+        left -= k;
+    }
 }
 
 // Entry of tag T in this band's part of the location array (only called at
@@ -225,6 +260,12 @@ static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t
             if (hv == c.n) ev_handler(S, K, V, c.n);
             else enq(S, K, c, KEV, hv, V, 1u);
         }
+        // memory nodes (R55): the victim is written back to its memory node
+        // as a B2 block (Table I "L2 Blk Replacement"), absorbed there
+        if (S.mem_mode && mem_node(S, V) != c.n) {
+            K.cnt(S, C_MEMWBSENT);
+            send_b2(S, K, c, mem_node(S, V), KTRAP, V | MEM_BIT);
+        }
     }
     uint4 nl = make_uint4(T + 1u, (uint32_t)t, (uint32_t)(t >> 32), 0u);
     record_access(S, l0 + victim, nl, c.n);   // a fresh residency: the installing access (R45)
@@ -264,15 +305,29 @@ __device__ __forceinline__ void complete(const Dev &S, const Sink &K, NodeCtx &c
 
 // core cold word w: install [0:2) (0 none, 1 install, 2 install and the
 // directory counted an EV of ours, NEXT-f2 R47) | rx << 2
+// A memory access of this core (install 0/1/2): off-mesh at the requester
+// (R17), or -- memory nodes (R55) -- a 1-flit request to the block's memory
+// node, whose B2 fill is followed by the memory latency here; a memory node
+// that is this node serves it locally
+__device__ __forceinline__ void mem_fetch(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t, uint32_t inst)
+{
+    K.cnt(S, C_MEMREQ);
+    load_cold(S, c);
+    c.cold.w = (c.cold.w & ~3u) | inst;
+    c.cold_dirty = true;
+    if (S.mem_mode && mem_node(S, c.cold.z) != c.n) {
+        enq(S, K, c, KDA, mem_node(S, c.cold.z), c.cold.z | MEM_BIT, 1u);
+        c.cold.w &= 3u;   // rx = 0
+        set_mode(c, MMEMFETCH, 0);
+        return;
+    }
+    set_mode(c, MMEMWAIT, t + S.mem_lat);
+}
+
 __device__ __forceinline__ void receive_ndr(const Dev &S, const Sink &K, NodeCtx &c, uint64_t t, uint32_t payload)
 {
     if (core_mode(c.hot) != MWAITDIR) atomicOr(S.err, ERR_PROTO);
-    K.cnt(S, C_MEMREQ);
-    load_cold(S, c);
-    const uint32_t inst = (payload & NDR_NOINSTALL) ? 0u : (payload & NDR_PEND) ? 2u : 1u;
-    c.cold.w = (c.cold.w & ~3u) | inst;
-    c.cold_dirty = true;
-    set_mode(c, MMEMWAIT, t + S.mem_lat);
+    mem_fetch(S, K, c, t, (payload & NDR_NOINSTALL) ? 0u : (payload & NDR_PEND) ? 2u : 1u);
 }
 
 __device__ __forceinline__ void receive_dr(const Dev &S, const Sink &K, NodeCtx &c, uint32_t holder)
@@ -334,6 +389,11 @@ static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint
     if (r == c.n) {
         if (kind == KNDR) receive_ndr(S, K, c, t, payload);
         else receive_dr(S, K, c, payload);
+    } else if (kind == KNDR && S.mem_mode == 1u) {
+        // memory at the directory (R55): the home hands the
+        // fetch to its memory and sends the B2 fill instead of the NDR
+        K.cnt(S, C_MEMFILLSENT);
+        send_b2(S, K, c, r, KRA, T | MEM_BIT);
     } else {
         enq(S, K, c, kind, r, payload, 1u);
     }
@@ -946,7 +1006,12 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
         else K.cnt(S, C_PROBES);
         break;
     case KDA:
-        dir_service(S, K, c, f.w, f_src(f), t);
+        if (f.w & MEM_BIT) {   // a memory request at a memory node (R55): the B2 fill
+            K.cnt(S, C_MEMFILLSENT);
+            send_b2(S, K, c, f_src(f), KRA, f.w);
+        } else {
+            dir_service(S, K, c, f.w, f_src(f), t);
+        }
         break;
     case KDR:
         receive_dr(S, K, c, f.w);
@@ -958,6 +1023,24 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
         serve_rq(S, K, c, f.w, f_src(f), t);
         break;
     case KRA: {
+        if (f.w & MEM_BIT) {   // a flit of a B2 memory fill (R55)
+            const uint32_t mode = core_mode(c.hot);
+            if (mode != MMEMFETCH && mode != MWAITDIR) atomicOr(S.err, ERR_PROTO);
+            load_cold(S, c);
+            if ((f.w & ~MEM_BIT) != c.cold.z) atomicOr(S.err, ERR_PROTO);
+            const uint32_t rx = (c.cold.w >> 2) + 1u;
+            c.cold_dirty = true;
+            if (rx == S.nfl_b2) {
+                K.cnt(S, C_MEMFILLRCVD);
+                uint32_t inst = c.cold.w & 3u;
+                if (mode == MWAITDIR) { K.cnt(S, C_MEMREQ); inst = 1u; }   // the home's memory answered (mem_mode 1)
+                c.cold.w = inst;
+                set_mode(c, MMEMWAIT, t + S.mem_lat);
+            } else {
+                c.cold.w = (c.cold.w & 3u) | (rx << 2);
+            }
+            break;
+        }
         if (core_mode(c.hot) != MWAITDATA) atomicOr(S.err, ERR_PROTO);
         load_cold(S, c);
         uint32_t rx = (c.cold.w >> 2) + 1u;
@@ -974,13 +1057,13 @@ static __device__ void phase3(const Dev &S, const Sink &K, NodeCtx &c, const Fli
         break;
     }
     case KTRAP:
+        if (f.w & MEM_BIT) {   // a memory writeback flit at a memory node: absorbed (R55)
+            K.cnt(S, C_MEMWBFLITS);
+            break;
+        }
         if (core_mode(c.hot) != MWAITDATA) atomicOr(S.err, ERR_PROTO);
         K.cnt(S, C_TRAPRCVD);
-        K.cnt(S, C_MEMREQ);
-        load_cold(S, c);
-        c.cold.w &= ~3u;                          // install = 0 (R16)
-        c.cold_dirty = true;
-        set_mode(c, MMEMWAIT, t + S.mem_lat);
+        mem_fetch(S, K, c, t, 0u);                // install = 0 (R16)
         break;
     default:  // KEV; with WB_BIT an L1 victim writeback, absorbed (R42)
         if (f.w & WB_BIT) K.cnt(S, C_WBRCVD);
@@ -1002,7 +1085,7 @@ __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t n
     if (qn == 0u || npresent - frees >= c.deg) return false;
     const uint32_t h = q_head(c.qctl);
     uint32_t nx = q_next(c.qctl);
-    if (!c.head_ok) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h]; c.head_ok = true; }
+    if (!c.head_ok) { c.head = fifo_of(S, c.l).p[h]; c.head_ok = true; }
     const uint2 p = c.head;
     const uint32_t nfl = (p.x >> 24) & 15u;
     out = f_make(p.x & NODE_MASK, (p.x >> 21) & 7u, nx, c.n, (uint32_t)t, p.y);
@@ -1010,10 +1093,11 @@ __device__ __forceinline__ bool inject_flit(const Dev &S, NodeCtx &c, uint32_t n
     ++acc.injected;
     ++nx;
     if (nx == nfl) {
-        const uint32_t h1 = (h + 1u) & (S.qcap - 1u);
+        const FifoRef F = fifo_of(S, c.l);
+        const uint32_t h1 = (h + 1u) & (F.cap - 1u);
         c.qctl = q_make(h1, qn - 1u, 0u);
         c.head_ok = qn > 1u;
-        if (c.head_ok) c.head = S.fifo_pkt[(size_t)c.l * S.qcap + h1];
+        if (c.head_ok) c.head = F.p[h1];
     } else {
         c.qctl = q_make(h, qn, nx);
     }

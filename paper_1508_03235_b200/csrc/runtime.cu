@@ -146,6 +146,13 @@ static int validate(const noc_sim_config *c)
     if (c->band_streams && (c->bands < 2 || c->world_size > 1 ||
                             (c->engine != NOC_ENGINE_TILED && c->engine != NOC_ENGINE_AUTO)))
         return fail(NOC_EINVAL, "band_streams needs bands >= 2 in one process and the TILED engine");
+    if (c->mem_mode > 2 || (c->mem_mode && (c->mode != NOC_MODE_LSPD || c->mig_hist || c->nfl_b2 < 1 || c->nfl_b2 > 16)))
+        return fail(NOC_EINVAL, "memory nodes (mem_mode 1/2) need LSPD mode, no migration and nfl_b2 1..16 (R54)");
+    if (c->mem_mode == 2 && (c->mem_ctrls < 1 || c->mem_ctrls > 64 || (c->mem_ctrls + 1) / 2 > c->mesh_w))
+        return fail(NOC_EINVAL, "mem_ctrls must be 1..64 with ceil(M/2) <= mesh_w");
+    if (c->hub_sendq_cap && (c->hub_sendq_cap < c->sendq_cap || c->hub_sendq_cap > 1024 ||
+                             (c->hub_sendq_cap & (c->hub_sendq_cap - 1))))
+        return fail(NOC_EINVAL, "hub_sendq_cap must be 0 or a power of two in sendq_cap..1024 (R56)");
     if (c->inject_mode && c->engine == NOC_ENGINE_TILED4)
         return fail(NOC_EINVAL, "inject_mode 1/2 (NEXT-f4) are not supported by the TILED4 engine");
     if (c->mode == NOC_MODE_LSPD && c->l1_sets &&
@@ -216,6 +223,9 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     D.age_base = cfg->age_base;
     D.mig_hist = cfg->mode == NOC_MODE_LSPD ? cfg->mig_hist : 0u;
     D.nfl_b2 = cfg->nfl_b2;
+    D.mem_mode = cfg->mode == NOC_MODE_LSPD ? cfg->mem_mode : 0u;
+    D.mem_ctrls = cfg->mem_ctrls;
+    D.hub_cap = cfg->hub_sendq_cap;
     D.sets = cfg->mode == NOC_MODE_LSPD ? cfg->l2_sets : 1u;
     D.ways = cfg->mode == NOC_MODE_LSPD ? cfg->l2_ways : 1u;
     D.tpn = cfg->mode == NOC_MODE_LSPD ? cfg->tags_per_node : 0u;
@@ -241,6 +251,21 @@ static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
     }
     if ((rc = dalloc(s, &D.fifo_ctl, n))) return rc;
     if ((rc = dalloc(s, &D.fifo_pkt, n * D.qcap))) return rc;
+    if (D.hub_cap) {
+        // hub nodes of this band (R56): the central directory node, the memory
+        // controllers; each gets a FIFO of hub_cap packets
+        std::vector<uint32_t> hubs;
+        if (D.dir_mode == 1u) hubs.push_back(D.dir_node);
+        if (D.mem_mode == 2u)
+            for (uint32_t k = 0; k < D.mem_ctrls; ++k) hubs.push_back(mem_ctrl_node(D.W, D.H, D.mem_ctrls, k));
+        std::vector<uint8_t> hub_of(n, 0);
+        uint32_t nh = 0;
+        for (uint32_t h : hubs)
+            if (h >= D.n0 && h < D.n0 + D.nloc && !hub_of[h - D.n0]) hub_of[h - D.n0] = (uint8_t)++nh;
+        if ((rc = dalloc(s, &D.hub_of, n))) return rc;
+        if ((rc = dalloc(s, &D.hub_pkt, (size_t)std::max<uint32_t>(nh, 1u) * D.hub_cap))) return rc;
+        CU(cudaMemcpy(D.hub_of, hub_of.data(), n, cudaMemcpyHostToDevice));
+    }
     if (cfg->mode == NOC_MODE_LSPD) {
         if ((rc = dalloc(s, &D.core_hot, n))) return rc;
         if ((rc = dalloc(s, &D.core_cold, n))) return rc;
@@ -775,6 +800,8 @@ extern "C" int noc_sim_stats(noc_sim *s, noc_sim_counters *out, uint64_t *hl, ui
         out->wb_received = (int64_t)c[C_WBRCVD];
         int64_t *mg = &out->mig_requests;
         for (int k = 0; k < 8; ++k) mg[k] = (int64_t)c[C_MIGREQ + k];
+        int64_t *mm = &out->mem_fills_sent;
+        for (int k = 0; k < 4; ++k) mm[k] = (int64_t)c[C_MEMFILLSENT + k];
     }
     uint64_t *hs[3] = {hl, hd, ha};
     for (int k = 0; k < 3; ++k)

@@ -165,7 +165,7 @@ k_tiled4(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t 
                 c.hot = S.core_hot[c.l];
                 c.cold = S.core_cold[c.l];
             }
-            if (q_count(c.qctl)) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + q_head(c.qctl)]; c.head_ok = true; }
+            if (q_count(c.qctl)) { c.head = fifo_of(S, c.l).p[q_head(c.qctl)]; c.head_ok = true; }
         }
         // port g's neighbour: slot in this tile, or LL receiver slot
         uint32_t m = c.l, mi = 0, w = 0;

@@ -357,7 +357,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             c.hot = S.core_hot[c.l];
             c.cold = S.core_cold[c.l];
         }
-        if (q_count(c.qctl)) { c.head = S.fifo_pkt[(size_t)c.l * S.qcap + q_head(c.qctl)]; c.head_ok = true; }
+        if (q_count(c.qctl)) { c.head = fifo_of(S, c.l).p[q_head(c.qctl)]; c.head_ok = true; }
         exist = (c.y > 0 ? 1u : 0u) | (c.y + 1 < S.H ? 2u : 0u) | (c.x + 1 < S.W ? 4u : 0u) | (c.x > 0 ? 8u : 0u);
         ext = ((lyy == 0 ? 1u : 0u) | (lyy + 1 == T.th ? 2u : 0u) | (lx + 1 == T.tw ? 4u : 0u) |
                (lx == 0 ? 8u : 0u)) & exist;
@@ -462,7 +462,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             const uint32_t m = wmask >> k;
             return m ? tc + (uint32_t)__ffs(m) : wbase + 32u;
         }
-        if (mode == MWAITDIR || mode == MWAITDATA) return tc;    // woken by Phase 3 only
+        if (mode == MWAITDIR || mode == MWAITDATA || mode == MMEMFETCH) return tc;   // woken by Phase 3 only
         return tc + ((c.hot - tc) & 0x1FFFFFFFu);                // the timer (ready mod 2^29)
     };
     const uint32_t pstride = 16u * S.nloc;

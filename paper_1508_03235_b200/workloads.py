@@ -16,6 +16,7 @@ MODE_UR, MODE_LSPD = 0, 1
 PRIO_DEFLECT, PRIO_OLDEST = 0, 1
 ROUTE_PMDR, ROUTE_XY = 0, 1   # NEXT-f4: strict XY + N,E,S,W deflection
 DIR_DISTRIBUTED, DIR_CENTRAL = 0, 1   # NEXT-f3: one node holds the whole directory
+MEM_OFFMESH, MEM_HOME, MEM_CTRLS = 0, 1, 2   # memory placement (R54): off-mesh, at the home node, controller nodes
 
 
 def thr(p) -> int:
@@ -32,7 +33,7 @@ BASE = dict(
     l2_hit_lat=1, mem_lat=100, nfl_ra=4,
     sendq_cap=16, hist_bins=4096, seed=1, route=0, dir_mode=0, dir_node=0,
     l1_sets=0, l1_ways=2, l1_miss_lat=2, inject_mode=0, age_base=0, band_streams=0,
-    mig_hist=0, nfl_b2=16,
+    mig_hist=0, nfl_b2=16, mem_mode=0, mem_ctrls=4, hub_sendq_cap=0,
 )
 
 

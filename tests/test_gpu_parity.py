@@ -558,3 +558,46 @@ def test_fill_all_c3_bands_and_tiled4_rejected():
     assert_same(g, o)
     with pytest.raises(nb.NocSimError):
         nb.NocSim(W.c1b(inject_mode=2), engine=nb.ENGINE_TILED4)
+
+
+MEM_CASES = {
+    "ctrl8x8": W.lspd(8, 8, lam=0.1, mem_mode=W.MEM_CTRLS, mem_ctrls=4, sendq_cap=64, hub_sendq_cap=256,
+                      l2_sets=4, seed=3, mem_lat=30),
+    "ctrl16x12_l1_xy": W.lspd(16, 12, lam=0.2, mem_mode=W.MEM_CTRLS, mem_ctrls=7, sendq_cap=64,
+                              hub_sendq_cap=1024, l2_sets=2, seed=5, mem_lat=20, l1_sets=2, l1_ways=2,
+                              route=W.ROUTE_XY, nfl_b2=5),
+    "home24x20": W.lspd(24, 20, lam=0.2, mem_mode=W.MEM_HOME, sendq_cap=64, l2_sets=2, seed=9, mem_lat=25,
+                        nfl_b2=8),
+    "central12x12": W.lspd(12, 12, lam=0.03, mem_mode=W.MEM_HOME, dir_mode=W.DIR_CENTRAL, dir_node=77,
+                           sendq_cap=16, hub_sendq_cap=1024, l2_sets=2, seed=2, mem_lat=15, nfl_b2=4),
+}
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("name", sorted(MEM_CASES))
+def test_memory_nodes_gpu(name, engine):
+    """Memory on the mesh (R54-R56): controller nodes with B2 fills and
+    writebacks, memory at the home / central directory node, hub FIFOs --
+    bit-exact against the oracle on every engine, with a drain."""
+    g, o = both(MEM_CASES[name], 2500, engine, split=[1, 999, 1500], drain=200000)
+    assert_same(g, o)
+    assert g.stats()[0]["mem_fills_received"] > 0
+
+
+def test_memory_nodes_c3_and_bands():
+    """C3 with memory at every home node (B2 fills and writebacks over the
+    whole mesh), in the bench's launch split; a 40x37 mesh with 6 memory
+    controllers and hub FIFOs as 3 and 5 virtual bands (the controllers of the
+    top and bottom rows live in different bands).  A handful of controllers
+    cannot serve C3: each ejects one flit per cycle, so its FIFO overflows."""
+    cfg = W.c3(mem_mode=W.MEM_HOME, sendq_cap=32)
+    g, o = both(cfg, 1200, split=[600, 600])
+    assert_same(g, o)
+    cfg = W.lspd(40, 37, lam=0.02, mem_mode=W.MEM_CTRLS, mem_ctrls=6, hub_sendq_cap=1024, sendq_cap=64)
+    for bands in (3, 5):
+        g = nb.NocSim(cfg, bands=bands, engine=nb.ENGINE_TILED)
+        o = Oracle(cfg)
+        for k in (7, 400, 993):
+            g.run(k)
+            o.run(k)
+        assert_same(g, o)

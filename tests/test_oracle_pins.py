@@ -46,7 +46,7 @@ def term(dom, idx, vals):
 
 
 LINK, FIFO, FIFONEXT, CORE, L2, LOC, CNT, HIST, CYCLE, SCRIPT, L1, L2MIG, LOCMIG, MIGRX = range(1, 15)
-IDLE, L2WAIT, WAIT_DIR, WAIT_DATA, MEMWAIT, L1WAIT = range(6)
+IDLE, L2WAIT, WAIT_DIR, WAIT_DATA, MEMWAIT, L1WAIT, MEMFETCH = range(7)
 
 
 def snapshot(o, cfg):
@@ -101,7 +101,8 @@ def design_hash(st, cfg):
         if nxt:
             terms.append(add(FIFONEXT, n, [nxt]))
     live = {L2WAIT: ("ready", "start"), WAIT_DIR: ("tag", "start"), WAIT_DATA: ("tag", "start", "rx"),
-            MEMWAIT: ("ready", "tag", "install", "start"), L1WAIT: ("ready", "tag", "start")}
+            MEMWAIT: ("ready", "tag", "install", "start"), L1WAIT: ("ready", "tag", "start"),
+            MEMFETCH: ("tag", "install", "start", "rx")}
     for n, c in st["core"].items():
         if c["mode"] == IDLE:
             continue
@@ -149,7 +150,7 @@ def design_hash(st, cfg):
     return H
 
 
-# counters in the order of DESIGN 3.6 (hash index 0..42)
+# counters in the order of DESIGN 3.6 (hash index 0..46)
 W_COUNTERS = ("generated", "packets_enqueued", "injected", "ejected", "hops", "deflections",
               "probes_delivered", "accesses", "completed", "l2_hits", "l2_misses",
               "dir_searches", "requests_made", "requests_received", "replies_sent",
@@ -158,7 +159,8 @@ W_COUNTERS = ("generated", "packets_enqueued", "injected", "ejected", "hops", "d
               "drops_probe", "drops_da", "drops_dr", "drops_ndr", "drops_rq", "drops_ra",
               "drops_trap", "drops_ev", "l1_hits", "l1_misses", "wb_sent", "wb_received",
               "mig_requests", "mig_nacks", "migrations", "mig_installs", "dir_updates", "invalidations",
-              "redirections", "rr_received")
+              "redirections", "rr_received",
+              "mem_fills_sent", "mem_fills_received", "mem_wbs_sent", "mem_wb_flits")
 
 
 def _busy_lspd(w, h, **kw):
@@ -177,6 +179,10 @@ HASH_CASES = {
     "lspd3x3_l1": _busy_lspd(3, 3, seed=5, l1_sets=1, l1_ways=2, l1_miss_lat=2),
     "lspd3x3_central": _busy_lspd(3, 3, seed=2, dir_mode=W.DIR_CENTRAL, dir_node=4),
     "lspd3x3_mig": _busy_lspd(3, 3, seed=6, mig_hist=3, nfl_b2=5, sendq_cap=64),
+    "lspd3x3_memctrl": _busy_lspd(3, 3, seed=4, mem_mode=W.MEM_CTRLS, mem_ctrls=2, nfl_b2=3,
+                                  sendq_cap=32, hub_sendq_cap=64),
+    "lspd3x3_memhome": _busy_lspd(3, 3, seed=8, mem_mode=W.MEM_HOME, nfl_b2=2, sendq_cap=32,
+                                  dir_mode=W.DIR_CENTRAL, dir_node=4, hub_sendq_cap=64),
 }
 
 
@@ -200,11 +206,14 @@ def test_state_hash_equals_design_definition(name):
         seen_domains["fifonext"] += sum(1 for nx, _ in st["fifo"].values() if nx)
         seen_domains["core"] += sum(1 for c in st["core"].values() if c["mode"])
         seen_domains["script"] += sum(1 for v in st["script"].values() if v)
+        seen_domains["memfetch"] += sum(1 for c in st["core"].values() if c["mode"] == MEMFETCH)
     assert seen_domains["link"] > 0 and seen_domains["fifo"] > 0
     if cfg["mode"] == W.MODE_LSPD:
         assert seen_domains["core"] > 0
     if name == "lspd3x3":
         assert seen_domains["script"] > 0
+    if name.startswith("lspd3x3_mem"):
+        assert seen_domains["memfetch"] > 0 or name == "lspd3x3_memhome"
 
 
 def _first(d, pred):
