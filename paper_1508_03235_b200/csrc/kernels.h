@@ -25,6 +25,8 @@ struct DevSet {
 // (sets S.TX, S.TY) within tiles_budget CTAs; tiled_prepare sets the launch
 // attributes for all bands' tiles in one cooperative launch
 bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np);
+// TILED kernel variant for a band: 0 UR, 1 lean LSPD, 2 full LSPD (tile_engine.cu)
+uint32_t tiled_kernel_mode(const Dev &D);
 cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
                           uint32_t *smem_hist);
 cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,

@@ -10,7 +10,19 @@
 #pragma once
 #include "common.cuh"
 
+// The lean TILED kernels (tile_m0.cu, tile_m1.cu define NOC_LEAN 1) compile
+// out the NEXT-f1 L1, NEXT-f2 migration and memory-node paths; the host runs
+// configurations that use any of them on the full kernels (tile_m2.cu and the
+// other engines), so the bench kernel carries none of their code.
+#ifndef NOC_LEAN
+#define NOC_LEAN 0
+#endif
+
 namespace noc {
+
+__device__ __forceinline__ uint32_t mig_on(const Dev &S) { return NOC_LEAN ? 0u : S.mig_hist; }
+__device__ __forceinline__ uint32_t mem_on(const Dev &S) { return NOC_LEAN ? 0u : S.mem_mode; }
+__device__ __forceinline__ uint32_t l1_on(const Dev &S) { return NOC_LEAN ? 0u : S.l1_sets; }
 
 // Statistic sink.  Rare counters / histogram bins go to shared memory (u32)
 // when the kernel provides it, else straight to global u64 atomics.
@@ -77,7 +89,7 @@ struct FifoRef {
 };
 __device__ __forceinline__ FifoRef fifo_of(const Dev &S, uint32_t l)
 {
-    if (S.hub_of) {
+    if (!NOC_LEAN && S.hub_of) {
         const uint32_t h = S.hub_of[l];
         if (h) return FifoRef{S.hub_pkt + (size_t)(h - 1u) * S.hub_cap, S.hub_cap};
     }
@@ -116,7 +128,7 @@ __device__ __forceinline__ uint32_t home_of(const Dev &S, uint32_t T)
 // The node holding block T's memory (R54): its home, or its controller
 __device__ __forceinline__ uint32_t mem_node(const Dev &S, uint32_t T)
 {
-    return S.mem_mode == 1u ? home_of(S, T) : mem_ctrl_node(S.W, S.H, S.mem_ctrls, T % S.mem_ctrls);
+    return mem_on(S) == 1u ? home_of(S, T) : mem_ctrl_node(S.W, S.H, S.mem_ctrls, T % S.mem_ctrls);
 }
 
 // A B2 block (Table I: nfl_b2 flits) of the given kind and payload to dst, as
@@ -146,11 +158,11 @@ __device__ __forceinline__ size_t loc_index(const Dev &S, uint32_t T)
 static __device__ __noinline__ uint32_t record_ring(const Dev &S, size_t li, uint32_t w, uint32_t who);
 __device__ __forceinline__ void record_access(const Dev &S, size_t li, uint4 &v, uint32_t who)
 {
-    if (S.mig_hist) v.w = record_ring(S, li, v.w, who);
+    if (mig_on(S)) v.w = record_ring(S, li, v.w, who);
 }
 static __device__ __noinline__ uint32_t record_ring(const Dev &S, size_t li, uint32_t vw, uint32_t who)
 {
-    const uint32_t N = S.mig_hist;
+    const uint32_t N = mig_on(S);
     uint32_t cnt = lw_count(vw), head = lw_head(vw);
     if (cnt < N) {
         S.l2h[li * N + (head + cnt) % N] = who;
@@ -199,7 +211,7 @@ __device__ __forceinline__ void ev_handler(const Dev &S, const Sink &K, uint32_t
     size_t i = loc_index(S, T);
     uint32_t e = S.loc[i];
     uint32_t h1 = e & HOLDER_MASK, pend = e >> HOLDER_BITS;
-    if (S.mig_hist) {
+    if (mig_on(S)) {
         const uint32_t m = S.loc_mig[i];
         if (m & 1u) {
             if (h1 != src + 1u) {
@@ -235,7 +247,7 @@ static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t
     uint32_t set = T % S.sets;
     const size_t l0 = ((size_t)c.l * S.sets + set) * S.ways;
     uint4 *L = S.l2 + l0;
-    if (S.mig_hist) drop_ghost(S, L, T);   // NEXT-f2: T lives here again
+    if (mig_on(S)) drop_ghost(S, L, T);   // NEXT-f2: T lives here again
     uint32_t victim = 0;
     uint64_t best = ~0ull;
     bool found_invalid = false;
@@ -262,7 +274,7 @@ static __device__ void install(const Dev &S, const Sink &K, NodeCtx &c, uint32_t
         }
         // memory nodes (R55): the victim is written back to its memory node
         // as a B2 block (Table I "L2 Blk Replacement"), absorbed there
-        if (S.mem_mode && mem_node(S, V) != c.n) {
+        if (mem_on(S) && mem_node(S, V) != c.n) {
             K.cnt(S, C_MEMWBSENT);
             send_b2(S, K, c, mem_node(S, V), KTRAP, V | MEM_BIT);
         }
@@ -315,7 +327,7 @@ __device__ __forceinline__ void mem_fetch(const Dev &S, const Sink &K, NodeCtx &
     load_cold(S, c);
     c.cold.w = (c.cold.w & ~3u) | inst;
     c.cold_dirty = true;
-    if (S.mem_mode && mem_node(S, c.cold.z) != c.n) {
+    if (mem_on(S) && mem_node(S, c.cold.z) != c.n) {
         enq(S, K, c, KDA, mem_node(S, c.cold.z), c.cold.z | MEM_BIT, 1u);
         c.cold.w &= 3u;   // rx = 0
         set_mode(c, MMEMFETCH, 0);
@@ -341,7 +353,7 @@ __device__ __forceinline__ void receive_dr(const Dev &S, const Sink &K, NodeCtx 
 
 static __device__ void l1_fill(const Dev &S, const Sink &K, NodeCtx &c, uint32_t T, uint32_t owner, uint64_t t)
 {
-    if (!S.l1_sets) return;
+    if (!l1_on(S)) return;
     uint4 *L = S.l1 + ((size_t)c.l * S.l1_sets + T % S.l1_sets) * S.l1_ways;
     uint32_t victim = 0;
     uint64_t best = ~0ull;
@@ -374,14 +386,14 @@ static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint
     uint32_t kind, payload;
     if (h1 == 0u) {
         h1 = r + 1u; kind = KNDR; payload = T;
-    } else if (h1 == r + 1u && S.mig_hist && (S.loc_mig[i] & 1u)) {
+    } else if (h1 == r + 1u && mig_on(S) && (S.loc_mig[i] & 1u)) {
         // NEXT-f2 (R47): r sent T away and dropped its copy; the block is on
         // its way to the target: r fetches from memory without installing
         kind = KNDR; payload = T | NDR_NOINSTALL;
     } else if (h1 == r + 1u) {
         ++pend;
         if (pend > PEND_MAX) { atomicOr(S.err, ERR_PEND); pend = PEND_MAX; }
-        kind = KNDR; payload = T | (S.mig_hist ? NDR_PEND : 0u);
+        kind = KNDR; payload = T | (mig_on(S) ? NDR_PEND : 0u);
     } else {
         kind = KDR; payload = h1 - 1u;
     }
@@ -389,7 +401,7 @@ static __device__ void dir_service(const Dev &S, const Sink &K, NodeCtx &c, uint
     if (r == c.n) {
         if (kind == KNDR) receive_ndr(S, K, c, t, payload);
         else receive_dr(S, K, c, payload);
-    } else if (kind == KNDR && S.mem_mode == 1u) {
+    } else if (kind == KNDR && mem_on(S) == 1u) {
         // memory at the directory (R55): the home hands the
         // fetch to its memory and sends the B2 fill instead of the NDR
         K.cnt(S, C_MEMFILLSENT);
@@ -417,7 +429,7 @@ __device__ __forceinline__ void ctl_enq(const Dev &S, const Sink &K, NodeCtx &c,
 // and strictly ahead of h; else 0xFFFFFFFF
 static __device__ uint32_t mig_target(const Dev &S, size_t li, uint32_t w, uint32_t h)
 {
-    const uint32_t N = S.mig_hist, cnt = lw_count(w), head = lw_head(w);
+    const uint32_t N = mig_on(S), cnt = lw_count(w), head = lw_head(w);
     const uint32_t *H = S.l2h + li * N;
     uint32_t best = 0xFFFFFFFFu, bestc = 0, hc = 0;
     for (uint32_t i = 0; i < cnt; ++i) {
@@ -567,10 +579,10 @@ static __device__ void serve_rq(const Dev &S, const Sink &K, NodeCtx &c, uint32_
         } else {
             enq(S, K, c, KRA, r, T, S.nfl_ra);
         }
-        if (S.mig_hist) maybe_migrate(S, K, c, T, l2_way(S, c, T));
+        if (mig_on(S)) maybe_migrate(S, K, c, T, l2_way(S, c, T));
         return;
     }
-    if (S.mig_hist && r != c.n && redirect(S, K, c, T, r)) return;
+    if (mig_on(S) && r != c.n && redirect(S, K, c, T, r)) return;
     K.cnt(S, C_TRAPSENT);
     if (r == c.n) {
         K.cnt(S, C_TRAPRCVD);
@@ -614,7 +626,7 @@ static __device__ void mem_fill(const Dev &S, const Sink &K, NodeCtx &c, uint64_
 {
     load_cold(S, c);
     const uint32_t T = c.cold.z;
-    if (S.mig_hist && l2_way(S, c, T) >= 0) {
+    if (mig_on(S) && l2_way(S, c, T) >= 0) {
         if ((c.cold.w & 3u) == 2u) {
             const uint32_t hv = home_of(S, T);
             K.cnt(S, C_EVSENT);
@@ -654,7 +666,7 @@ static __device__ void start_access(const Dev &S, const Sink &K, NodeCtx &c, uin
     c.cold = make_uint4((uint32_t)t, (uint32_t)(t >> 32), T, 0u);   // start, tag, install 0, rx 0
     c.cold_dirty = true;
     K.cnt(S, C_ACCESSES);
-    if (S.l1_sets) {
+    if (l1_on(S)) {
         if (l1_hit(S, c, T, t)) {
             K.cnt(S, C_L1HIT);
             complete(S, K, c, t);

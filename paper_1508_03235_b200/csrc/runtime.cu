@@ -477,7 +477,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         }
         cudaError_t ce = cudaErrorInvalidConfiguration;
         if (ok) ce = four ? tiled4_prepare(cfg->mode, cfg->hist_bins, np, total, s->device, &s->t_smem_hist)
-                          : tiled_prepare(cfg->mode == NOC_MODE_LSPD && cfg->l1_sets ? 2u : cfg->mode,
+                          : tiled_prepare(tiled_kernel_mode(s->D[0]),
                                           cfg->route | (cfg->inject_mode ? 2u : 0u) | (s->nb > 1 || s->world > 1 ? 4u : 0u),
                                           cfg->hist_bins, np, total, s->device, &s->t_smem_hist);
         if (ce == cudaSuccess) {

@@ -114,7 +114,13 @@ bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np)
 
 // Shared-memory attribute and co-residency check for one launch of
 // total_tiles CTAs of np threads.
-// kernel mode: 0 UR, 1 LSPD, 2 LSPD with the private L1; feat: FEAT bits
+// kernel mode: 0 UR, 1 LSPD (lean: NOC_LEAN), 2 LSPD with the private L1,
+// migration, memory nodes or hub FIFOs (full); feat: FEAT bits
+uint32_t tiled_kernel_mode(const Dev &D)
+{
+    if (D.mode != 1u) return D.mode;
+    return (D.l1_sets || D.mig_hist || D.mem_mode || D.hub_cap) ? 2u : 1u;
+}
 static const void *tiled_fn(uint32_t mode, bool drain, uint32_t feat)
 {
 #define NOC_TD(M, F) (drain ? (const void *)k_tiled<M, true, F> : (const void *)k_tiled<M, false, F>)
@@ -170,7 +176,7 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     size_t smem = tiled_smem_bytes(P.d[0], tpad, smem_hist != 0);
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
     const bool dr = activity != nullptr;
-    const void *fn = tiled_fn(P.d[0].mode == 1u && P.d[0].l1_sets ? 2u : P.d[0].mode, dr,
+    const void *fn = tiled_fn(tiled_kernel_mode(P.d[0]), dr,
                               P.d[0].route | (P.d[0].inject_mode ? 2u : 0u) | (P.general ? 4u : 0u));
     // the dynamic shared-memory limit is a per-function (process-wide)
     // attribute: another handle of a different size may have lowered it

@@ -1,5 +1,6 @@
 // tile_m0.cu -- instantiations of the TILED kernel for traffic mode 0
 // (uniform random); the kernel is tile_kernel.cuh, the host side tile_engine.cu.
+#define NOC_LEAN 1   // node_logic.cuh: no L1 / migration / memory-node code
 #include "tile_kernel.cuh"
 
 namespace noc {

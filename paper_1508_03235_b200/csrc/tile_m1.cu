@@ -1,6 +1,7 @@
 // tile_m1.cu -- instantiations of the TILED kernel for traffic mode 1
 // (LSPD); the kernel is tile_kernel.cuh, the host side tile_engine.cu.
 #define NOC_TRACE_OWNER
+#define NOC_LEAN 1   // node_logic.cuh: no L1 / migration / memory-node code
 #include "tile_kernel.cuh"
 
 namespace noc {
