@@ -231,6 +231,22 @@ int noc_sim_nccl_unique_id(uint8_t out[128]);
  * NOC_ECUDA, NOC_ENCCL.  On error *out = NULL. */
 int noc_sim_create(const noc_sim_config *cfg, noc_sim **out);
 
+/* NEXT-f3 streamed trace replay (DESIGN R57; SURVEY f3 "streamed with
+ * double-buffered chunked H2D copies instead of the paper's per-cycle
+ * cudaMemcpy"): append scripted generation events (the same
+ * records as noc_sim_config.script) to the nodes' queues, so traces larger
+ * than device memory are replayed chunk by chunk.  ev: host array of n events,
+ * copied before the call returns (pinned staging; the host-to-device copy runs
+ * asynchronously and overlaps the next noc_sim_run when none of the chunk's
+ * events is due in it).  Per node the pushed events are ordered by cycle
+ * (stable, as at create) and must not precede the node's earlier events.
+ * Consumed events are dropped from device memory at the next merge.  Results
+ * equal those of the whole script given at create as long as every event is
+ * pushed before it is due.  With world_size > 1 every rank pushes the same
+ * events (each keeps its band's).  Errors: NOC_EINVAL (range or order),
+ * NOC_ECUDA, NOC_ESTATE (poisoned handle). */
+int noc_sim_push_script(noc_sim *sim, const noc_sim_event *ev, uint64_t n);
+
 /* Advance exactly n_cycles cycles (the while loop of P:L275-284 without its
  * per-cycle trace copy).  Resumable: run(a); run(b) == run(a+b).  Blocks until
  * the device finished.  Collective when world_size > 1.

@@ -87,6 +87,7 @@ def lib():
         L.orc_set_debug.argtypes = [C.c_void_p, C.c_int]
         L.orc_run.argtypes = [C.c_void_p, C.c_uint64]
         L.orc_drain.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
+        L.orc_push_script.argtypes = [C.c_void_p, C.POINTER(_Event), C.c_uint64]
         L.orc_stats.argtypes = [C.c_void_p, C.POINTER(_Counters), C.c_void_p, C.c_void_p,
                                 C.c_void_p, C.c_uint32]
         L.orc_state_hash.argtypes = [C.c_void_p]
@@ -203,6 +204,14 @@ class Oracle:
 
     def run(self, n_cycles: int):
         _check(lib().orc_run(self._h, int(n_cycles)))
+
+    def push_script(self, events):
+        """Append scripted events [(cycle, node, value), ...] (R57)."""
+        events = list(events)
+        ev = (_Event * max(len(events), 1))()
+        for i, (cy, node, val) in enumerate(events):
+            ev[i].cycle, ev[i].node, ev[i].value = cy, node, val
+        _check(lib().orc_push_script(self._h, ev, len(events)))
 
     def drain(self, max_cycles: int):
         used = C.c_uint64()

@@ -95,6 +95,7 @@ typedef struct {
     L1Line *l1;        /* Core.L1 (NEXT-f1), l1_sets x l1_ways                 */
     uint64_t script_pos, script_end;
     uint64_t script_used;
+    uint64_t script_last;  /* cycle of the node's last scripted event so far (pushes, R57) */
     struct { uint32_t tag, count; int used; } migrx[4];   /* inbound B2 reassembly (R52) */
 } Node;
 
@@ -109,6 +110,7 @@ struct orc_sim {
     LocEntry *loc;
     uint64_t ntags;
     orc_event *script;
+    uint64_t n_script;
     orc_counters c;
     uint64_t *hl, *hd, *ha;
     int gen_enabled;
@@ -1339,11 +1341,76 @@ int orc_create(const orc_config *cfg, orc_sim **out)
         uint64_t i = 0;
         for (uint64_t n = 0; n < N; ++n) {
             s->nodes[n].script_pos = i;
-            while (i < cfg->n_script && s->script[i].node == n) ++i;
+            while (i < cfg->n_script && s->script[i].node == n) s->nodes[n].script_last = s->script[i++].cycle;
             s->nodes[n].script_end = i;
         }
     }
+    s->n_script = cfg->n_script;
     *out = s;
+    return ORC_OK;
+}
+
+static int check_event(const orc_sim *s, const orc_event *e)
+{
+    if (e->node >= s->N) { set_err("script node out of range"); return ORC_EINVAL; }
+    if (s->cfg.mode == ORC_MODE_UR && (e->value >= s->N || e->value == e->node)) {
+        set_err("script probe destination invalid"); return ORC_EINVAL;
+    }
+    if (s->cfg.mode == ORC_MODE_LSPD && (uint64_t)e->value >= (uint64_t)s->cfg.tags_per_node * s->N) {
+        set_err("script tag out of range"); return ORC_EINVAL;
+    }
+    return ORC_OK;
+}
+
+/* NEXT-f3 streamed trace replay (R57): append events to the nodes' script
+ * queues.  The pushed events are ordered per node by cycle (stable, as at
+ * create); a node's first pushed event may not be earlier than its last event
+ * so far, so each node's queue stays ordered and a script pushed in pieces
+ * before its events are due behaves as the whole script given at create.
+ * Consumed events are dropped (the queues hold only what is still to come). */
+int orc_push_script(orc_sim *s, const orc_event *ev, uint64_t n)
+{
+    if (s->err) return s->err;
+    if (n && !ev) { set_err("null events"); return ORC_EINVAL; }
+    orc_event *add = malloc((n ? n : 1) * sizeof(orc_event));
+    uint64_t *cnt = calloc(s->N + 1, sizeof(uint64_t));
+    if (!add || !cnt) { free(add); free(cnt); set_err("out of memory"); return ORC_ENOMEM; }
+    for (uint64_t i = 0; i < n; ++i) {
+        int rc = check_event(s, &ev[i]);
+        if (rc) { free(add); free(cnt); return rc; }
+        orc_event e = ev[i];                      /* stable insertion sort by (node, cycle) */
+        uint64_t j = i;
+        while (j > 0 && cmp_event(&e, &add[j - 1]) < 0) { add[j] = add[j - 1]; --j; }
+        add[j] = e;
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        const Node *c = &s->nodes[add[i].node];
+        int first = i == 0 || add[i - 1].node != add[i].node;
+        if (first && (c->script_used || c->script_end > c->script_pos) && add[i].cycle < c->script_last) {
+            free(add); free(cnt);
+            set_err("pushed events of a node must not precede its earlier events");
+            return ORC_EINVAL;
+        }
+        cnt[add[i].node] += 1;
+    }
+    uint64_t total = n;
+    for (uint32_t v = 0; v < s->N; ++v) total += s->nodes[v].script_end - s->nodes[v].script_pos;
+    orc_event *ns = malloc((total ? total : 1) * sizeof(orc_event));
+    if (!ns) { free(add); free(cnt); set_err("out of memory"); return ORC_ENOMEM; }
+    uint64_t k = 0, a = 0;
+    for (uint32_t v = 0; v < s->N; ++v) {
+        Node *c = &s->nodes[v];
+        const uint64_t p0 = k;
+        for (uint64_t i = c->script_pos; i < c->script_end; ++i) ns[k++] = s->script[i];   /* still to come */
+        for (uint64_t i = 0; i < cnt[v]; ++i) { ns[k] = add[a++]; c->script_last = ns[k].cycle; ++k; }
+        c->script_pos = p0;
+        c->script_end = k;
+    }
+    free(s->script);
+    s->script = ns;
+    s->n_script = total;
+    free(add);
+    free(cnt);
     return ORC_OK;
 }
 

@@ -109,6 +109,9 @@ void orc_destroy(orc_sim *s);
 int  orc_set_debug(orc_sim *s, int flags);
 int  orc_run(orc_sim *s, uint64_t n_cycles);
 int  orc_drain(orc_sim *s, uint64_t max_cycles, uint64_t *used, int *drained);
+/* NEXT-f3 streamed trace replay (R57): append script events (copied); per node
+ * ordered by cycle, not earlier than the node's previous events (ORC_EINVAL). */
+int  orc_push_script(orc_sim *s, const orc_event *ev, uint64_t n);
 int  orc_stats(const orc_sim *s, orc_counters *out, uint64_t *hist_lat,
                uint64_t *hist_defl, uint64_t *hist_acc, uint32_t nbins);
 uint64_t orc_state_hash(const orc_sim *s);

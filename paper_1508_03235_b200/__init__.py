@@ -95,6 +95,7 @@ def lib():
         L.noc_sim_run.argtypes = [P, C.c_uint64]
         L.noc_sim_run_timed.argtypes = [P, C.c_uint64, C.POINTER(C.c_double)]
         L.noc_sim_drain.argtypes = [P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
+        L.noc_sim_push_script.argtypes = [P, C.POINTER(noc_sim_event), C.c_uint64]
         L.noc_sim_stats.argtypes = [P, C.POINTER(noc_sim_counters), P, P, P, C.c_uint32]
         L.noc_sim_state_hash.argtypes = [P, C.POINTER(C.c_uint64)]
         L.noc_sim_get_info.argtypes = [P, C.POINTER(noc_sim_info)]
@@ -218,6 +219,15 @@ class NocSim:
 
     def run_timed(self, n):
         return noc_sim_run_timed(self._h, n)
+
+    def push_script(self, events):
+        """Append scripted events [(cycle, node, value), ...] (NEXT-f3 streamed
+        trace replay, noc_sim_push_script, DESIGN R57)."""
+        events = list(events)
+        ev = (noc_sim_event * max(len(events), 1))()
+        for i, (cy, node, val) in enumerate(events):
+            ev[i].cycle, ev[i].node, ev[i].value = cy, node, val
+        _check(lib().noc_sim_push_script(self._h, ev, len(events)))
 
     def drain(self, max_cycles):
         return noc_sim_drain(self._h, max_cycles)

@@ -216,6 +216,8 @@ struct Dev {
     const uint4 *script;              // [n_script] {cycle_lo, cycle_hi, value, 0} grouped by node
     const uint32_t *script_off;       // [nloc+1]
     uint32_t *script_pos;             // [nloc] events consumed
+    uint32_t *script_base;            // [nloc] events consumed before the last merge of pushed
+                                      // events (NEXT-f3 streaming, R57); null = 0
     unsigned long long *cnt;          // [NCOUNTERS]
     unsigned long long *hist;         // [3][nb]
     uint32_t *err;                    // [1] error flags

@@ -149,11 +149,32 @@ __global__ void __launch_bounds__(PERSIST_BLOCK, PERSIST_MIN_BLOCKS) k_persist(c
         for (uint32_t l = lo_node + threadIdx.x; l < hi_node; l += blockDim.x) {
 #ifndef NOC_NO_PERSIST_PREFETCH
             const uint32_t ln = l + blockDim.x;
+#if defined(NOC_AB_PF4) || defined(NOC_AB_PF2)
+            if (ln < hi_node) {
+                const uint32_t pb = (uint32_t)t & 1u;
+#pragma unroll
+                for (uint32_t d = 0; d < 4; ++d) prefetch_l1(&S.flit[pb][(size_t)d * S.nloc + ln]);
+            }
+#endif
+#ifdef NOC_AB_PF2
+            const uint32_t ln2 = ln + blockDim.x;
+            if (ln2 < hi_node) {
+                prefetch_l1(&S.flag[(uint32_t)t & 1u][ln2]);
+                prefetch_l1(&S.fifo_ctl[ln2]);
+                if (MODE == 1u) prefetch_l1(&S.core_hot[ln2]);
+            }
+            if (l == lo_node + threadIdx.x && ln < hi_node) {
+                prefetch_l1(&S.flag[(uint32_t)t & 1u][ln]);
+                prefetch_l1(&S.fifo_ctl[ln]);
+                if (MODE == 1u) prefetch_l1(&S.core_hot[ln]);
+            }
+#else
             if (ln < hi_node) {
                 prefetch_l1(&S.flag[(uint32_t)t & 1u][ln]);
                 prefetch_l1(&S.fifo_ctl[ln]);
                 if (MODE == 1u) prefetch_l1(&S.core_hot[ln]);
             }
+#endif
 #endif
             busy |= node_step_global<MODE>(S, K, l, t, acc);
         }
@@ -202,6 +223,43 @@ __device__ bool read_slot(const Dev &S, uint32_t l, uint32_t d, uint64_t t, Flit
     uint4 v = S.flit[b][(size_t)d * S.nloc + l];
     f = Flit{v.x, v.y, v.z, v.w};
     return true;
+}
+
+// ------------------------------------------------------------------ streamed scripts (R57)
+// Per node: events still to come = the old queue minus the consumed ones,
+// then the pushed ones (add_off / add_ev: this band's pushed events by node).
+__global__ void k_script_count(Dev S, const uint32_t *add_off, uint32_t *cnt)
+{
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= S.nloc) return;
+    const uint32_t base = S.script_base ? S.script_base[l] : 0u;
+    const uint32_t rem = S.script_off[l + 1] - S.script_off[l] - (S.script_pos[l] - base);
+    cnt[l] = rem + add_off[l + 1] - add_off[l];
+}
+
+__global__ void k_script_merge(Dev S, const uint32_t *add_off, const uint4 *add_ev, const uint32_t *new_off,
+                               uint4 *new_ev, uint32_t *new_base)
+{
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= S.nloc) return;
+    const uint32_t pos = S.script_pos[l], base = S.script_base ? S.script_base[l] : 0u;
+    uint32_t k = new_off[l];
+    for (uint32_t i = S.script_off[l] + pos - base; i < S.script_off[l + 1]; ++i) new_ev[k++] = S.script[i];
+    for (uint32_t i = add_off[l]; i < add_off[l + 1]; ++i) new_ev[k++] = add_ev[i];
+    new_base[l] = pos;
+}
+
+cudaError_t launch_script_count(const Dev &S, const uint32_t *add_off, uint32_t *cnt, cudaStream_t st)
+{
+    k_script_count<<<(S.nloc + 255) / 256, 256, 0, st>>>(S, add_off, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_script_merge(const Dev &S, const uint32_t *add_off, const uint4 *add_ev, const uint32_t *new_off,
+                                uint4 *new_ev, uint32_t *new_base, cudaStream_t st)
+{
+    k_script_merge<<<(S.nloc + 255) / 256, 256, 0, st>>>(S, add_off, add_ev, new_off, new_ev, new_base);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ drain helper

@@ -27,6 +27,10 @@ struct DevSet {
 bool tiled_plan(Dev &S, uint32_t tiles_budget, uint32_t *tiles, uint32_t *np);
 // TILED kernel variant for a band: 0 UR, 1 lean LSPD, 2 full LSPD (tile_engine.cu)
 uint32_t tiled_kernel_mode(const Dev &D);
+// streamed scripts (NEXT-f3, R57): per-node counts and the merge of pushed events
+cudaError_t launch_script_count(const Dev &S, const uint32_t *add_off, uint32_t *cnt, cudaStream_t st);
+cudaError_t launch_script_merge(const Dev &S, const uint32_t *add_off, const uint4 *add_ev, const uint32_t *new_off,
+                                uint4 *new_ev, uint32_t *new_base, cudaStream_t st);
 cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
                           uint32_t *smem_hist);
 cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,

@@ -684,8 +684,11 @@ __device__ __forceinline__ bool script_next(const Dev &S, const NodeCtx &c, uint
 {
     uint32_t off = S.script_off[c.l], end = S.script_off[c.l + 1];
     uint32_t pos = S.script_pos[c.l];
-    if (off + pos >= end) return false;
-    uint4 ev = S.script[off + pos];
+    // pushed events (R57): the queue holds only events not consumed at the
+    // last merge, so the next one sits at pos - base
+    const uint32_t idx = off + pos - (S.script_base ? S.script_base[c.l] : 0u);
+    if (idx >= end) return false;
+    uint4 ev = S.script[idx];
     uint64_t cyc = ((uint64_t)ev.y << 32) | ev.x;
     if (cyc > t) return false;
     value = ev.z;

@@ -84,7 +84,23 @@ struct noc_sim {
     cudaEvent_t mev = nullptr;
     DevSet bset[MAX_BANDS];
     std::vector<void *> allocs;
+    std::vector<size_t> alloc_bytes;
     uint64_t bytes = 0, loc_bytes = 0;
+    // streamed scripts (NEXT-f3, R57): per node the cycle of its last event so
+    // far; pushed chunks waiting to be merged (per band: device staging filled
+    // by an asynchronous copy on cstream from pinned host memory)
+    std::vector<uint64_t> script_last;
+    std::vector<uint8_t> script_any;
+    struct Pending {
+        uint64_t min_cycle;
+        uint32_t n[MAX_BANDS];
+        uint4 *ev[MAX_BANDS];
+        uint32_t *off[MAX_BANDS];
+        void *host;
+        cudaEvent_t done;
+    };
+    std::vector<Pending> pending;
+    cudaStream_t cstream = nullptr;
     uint64_t launches = 0;
     int sm_count = 0;
     int poisoned = 0;
@@ -103,9 +119,23 @@ static int dalloc(noc_sim *s, T **p, size_t count)
     e = cudaMemset(q, 0, b);
     if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("cudaMemset: ") + cudaGetErrorString(e));
     s->allocs.push_back(q);
+    s->alloc_bytes.push_back(b);
     s->bytes += b;
     *p = (T *)q;
     return NOC_OK;
+}
+
+// free one dalloc'ed buffer (streamed-script arrays that are replaced)
+static void dfree(noc_sim *s, void *p)
+{
+    for (size_t i = 0; i < s->allocs.size(); ++i)
+        if (s->allocs[i] == p) {
+            cudaFree(p);
+            s->bytes -= s->alloc_bytes[i];
+            s->allocs.erase(s->allocs.begin() + (long)i);
+            s->alloc_bytes.erase(s->alloc_bytes.begin() + (long)i);
+            return;
+        }
 }
 
 static int validate(const noc_sim_config *c)
@@ -180,6 +210,11 @@ extern "C" void noc_sim_destroy(noc_sim *s)
     for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
     if (s->comm) ncclCommDestroy(s->comm);
     for (void *p : s->allocs) cudaFree(p);
+    for (auto &pd : s->pending) {
+        if (pd.host) cudaFreeHost(pd.host);
+        if (pd.done) cudaEventDestroy(pd.done);
+    }
+    if (s->cstream) { cudaStreamSynchronize(s->cstream); cudaStreamDestroy(s->cstream); }
     for (int k = 0; k < MAX_BANDS; ++k) {
         if (s->bst[k]) { cudaStreamSynchronize(s->bst[k]); cudaStreamDestroy(s->bst[k]); }
         if (s->bev[k]) cudaEventDestroy(s->bev[k]);
@@ -558,6 +593,19 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
         }
         for (int k = 0; k < s->nb; ++k) s->set.d[k] = s->D[k];
     }
+    // streamed scripts (R57): the last create-time event cycle of every node
+    {
+        const uint64_t N = (uint64_t)cfg->mesh_w * cfg->mesh_h;
+        s->script_last.assign(N, 0);
+        s->script_any.assign(N, 0);
+        for (uint64_t i = 0; i < cfg->n_script; ++i) {
+            const noc_sim_event &x = cfg->script[i];
+            if (!s->script_any[x.node] || x.cycle > s->script_last[x.node]) s->script_last[x.node] = x.cycle;
+            s->script_any[x.node] = 1;
+        }
+        if (cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(NOC_ECUDA, "copy stream creation failed"));
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(NOC_ECUDA, "init sync failed"));
     if (s->world > 1) {   // every rank has mapped its neighbours before anyone runs
         if ((rc = allreduce_u32(s, s->d_scratch, 1))) return bail(rc);
@@ -587,6 +635,57 @@ static int check_err(noc_sim *s)
     return NOC_OK;
 }
 
+// Refresh the launch sets' copies of band k's view after a host-side change
+static void sync_band_views(noc_sim *s, int k)
+{
+    s->set.d[k] = s->D[k];
+    if (s->split) s->bset[k].d[0] = s->D[k];
+}
+
+// Merge the pushed script chunks into the bands' event queues (R57): per node
+// the events not consumed yet, then the pushed ones; consumed events are
+// dropped, so device memory holds only what is still to come.
+static int merge_scripts(noc_sim *s)
+{
+    for (auto &pd : s->pending) {
+        CU(cudaStreamWaitEvent(s->stream, pd.done, 0));
+        for (int k = 0; k < s->nb; ++k) {
+            Dev &D = s->D[k];
+            const size_t n = D.nloc;
+            uint32_t *cnt = nullptr, *new_off = nullptr, *new_base = nullptr;
+            int rc;
+            if ((rc = dalloc(s, &cnt, n))) return rc;
+            CU(launch_script_count(D, pd.off[k], cnt, s->stream));
+            std::vector<uint32_t> h(n), off(n + 1, 0);
+            CU(cudaMemcpyAsync(h.data(), cnt, n * 4, cudaMemcpyDeviceToHost, s->stream));
+            CU(cudaStreamSynchronize(s->stream));
+            for (size_t l = 0; l < n; ++l) off[l + 1] = off[l] + h[l];
+            uint4 *new_ev = nullptr;
+            if ((rc = dalloc(s, &new_off, n + 1))) return rc;
+            if ((rc = dalloc(s, &new_base, n))) return rc;
+            if ((rc = dalloc(s, &new_ev, off[n]))) return rc;
+            CU(cudaMemcpyAsync(new_off, off.data(), (n + 1) * 4, cudaMemcpyHostToDevice, s->stream));
+            CU(launch_script_merge(D, pd.off[k], pd.ev[k], new_off, new_ev, new_base, s->stream));
+            CU(cudaStreamSynchronize(s->stream));
+            dfree(s, (void *)D.script);
+            dfree(s, (void *)D.script_off);
+            if (D.script_base) dfree(s, D.script_base);
+            dfree(s, cnt);
+            dfree(s, pd.ev[k]);
+            dfree(s, pd.off[k]);
+            D.script = new_ev;
+            D.script_off = new_off;
+            D.script_base = new_base;
+            D.has_script = 1;
+            sync_band_views(s, k);
+        }
+        cudaFreeHost(pd.host);
+        cudaEventDestroy(pd.done);
+    }
+    s->pending.clear();
+    return NOC_OK;
+}
+
 static void set_gen(noc_sim *s, uint32_t gen)
 {
     for (int k = 0; k < s->nb; ++k) {
@@ -598,7 +697,28 @@ static void set_gen(noc_sim *s, uint32_t gen)
 
 // Advance n cycles with the handle's engine; activity (device, may be null)
 // receives per-cycle busy-CTA counts when draining (n <= DRAIN_CHUNK).
+static int advance_launches(noc_sim *s, uint64_t n, uint32_t *activity);
+
 static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
+{
+    // pushed script chunks (R57): merged before the launches if any of their
+    // events may be due in this run, else after them (their copy overlaps it)
+    if (!s->pending.empty()) {
+        uint64_t due = ~0ull;
+        for (auto &pd : s->pending) due = std::min(due, pd.min_cycle);
+        if (due < s->t + n) {
+            int rc = merge_scripts(s);
+            if (rc) return rc;
+        } else {
+            int rc = advance_launches(s, n, activity);
+            if (rc) return rc;
+            return merge_scripts(s);
+        }
+    }
+    return advance_launches(s, n, activity);
+}
+
+static int advance_launches(noc_sim *s, uint64_t n, uint32_t *activity)
 {
     cudaError_t e;
     if (s->split) {
@@ -676,6 +796,82 @@ static int advance(noc_sim *s, uint64_t n, uint32_t *activity)
         }
     }
     s->t += n;
+    return NOC_OK;
+}
+
+extern "C" int noc_sim_push_script(noc_sim *s, const noc_sim_event *ev, uint64_t n)
+{
+    if (!s) return fail(NOC_EINVAL, "null handle");
+    if (s->poisoned) return fail(NOC_ESTATE, "handle poisoned by an earlier error");
+    if (n && !ev) return fail(NOC_EINVAL, "null events");
+    if (!n) return NOC_OK;
+    const noc_sim_config *c = &s->cfg;
+    const uint64_t N = (uint64_t)c->mesh_w * c->mesh_h;
+    std::vector<uint64_t> idx(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        const noc_sim_event &e = ev[i];
+        if (e.node >= N) return fail(NOC_EINVAL, "script node out of range");
+        if (c->mode == NOC_MODE_UR && (e.value >= N || e.value == e.node))
+            return fail(NOC_EINVAL, "script probe destination invalid");
+        if (c->mode == NOC_MODE_LSPD && (uint64_t)e.value >= (uint64_t)c->tags_per_node * N)
+            return fail(NOC_EINVAL, "script tag out of range");
+        idx[i] = i;
+    }
+    std::stable_sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
+        if (ev[a].node != ev[b].node) return ev[a].node < ev[b].node;
+        return ev[a].cycle < ev[b].cycle;
+    });
+    for (uint64_t i = 0; i < n; ++i) {   // each node's queue stays ordered by cycle
+        const noc_sim_event &e = ev[idx[i]];
+        if ((i == 0 || ev[idx[i - 1]].node != e.node) && s->script_any[e.node] && e.cycle < s->script_last[e.node])
+            return fail(NOC_EINVAL, "pushed events of a node must not precede its earlier events");
+    }
+    CU(cudaSetDevice(s->device));
+    noc_sim::Pending pd{};
+    pd.min_cycle = ~0ull;
+    // pinned staging: per band the events (by node) and the per-node offsets
+    size_t host_bytes = 0;
+    std::vector<std::vector<uint4>> bev(s->nb);
+    std::vector<std::vector<uint32_t>> boff(s->nb);
+    for (int k = 0; k < s->nb; ++k) {
+        const Dev &D = s->D[k];
+        boff[k].assign(D.nloc + 1, 0);
+        for (uint64_t i = 0; i < n; ++i) {
+            const noc_sim_event &e = ev[idx[i]];
+            if (e.node < D.n0 || e.node >= D.n0 + D.nloc) continue;
+            bev[k].push_back(make_uint4((uint32_t)e.cycle, (uint32_t)(e.cycle >> 32), e.value, 0u));
+            boff[k][e.node - D.n0 + 1] += 1;
+        }
+        for (uint32_t l = 0; l < D.nloc; ++l) boff[k][l + 1] += boff[k][l];
+        host_bytes += bev[k].size() * sizeof(uint4) + boff[k].size() * 4;
+    }
+    CU(cudaMallocHost(&pd.host, std::max<size_t>(host_bytes, 16)));
+    CU(cudaEventCreateWithFlags(&pd.done, cudaEventDisableTiming));
+    uint8_t *hp = (uint8_t *)pd.host;
+    for (int k = 0; k < s->nb; ++k) {
+        int rc;
+        pd.n[k] = (uint32_t)bev[k].size();
+        if ((rc = dalloc(s, &pd.ev[k], bev[k].size()))) return rc;
+        if ((rc = dalloc(s, &pd.off[k], boff[k].size()))) return rc;
+        memcpy(hp, bev[k].data(), bev[k].size() * sizeof(uint4));
+        CU(cudaMemcpyAsync(pd.ev[k], hp, bev[k].size() * sizeof(uint4), cudaMemcpyHostToDevice, s->cstream));
+        hp += bev[k].size() * sizeof(uint4);
+        memcpy(hp, boff[k].data(), boff[k].size() * 4);
+        CU(cudaMemcpyAsync(pd.off[k], hp, boff[k].size() * 4, cudaMemcpyHostToDevice, s->cstream));
+        hp += boff[k].size() * 4;
+    }
+    CU(cudaEventRecord(pd.done, s->cstream));
+    for (uint64_t i = 0; i < n; ++i) {
+        const noc_sim_event &e = ev[idx[i]];
+        s->script_last[e.node] = e.cycle;     // ordered by cycle within a node
+        s->script_any[e.node] = 1;
+        pd.min_cycle = std::min(pd.min_cycle, e.cycle);
+    }
+    for (int k = 0; k < s->nb; ++k) {
+        s->D[k].has_script = 1;
+        sync_band_views(s, k);
+    }
+    s->pending.push_back(pd);
     return NOC_OK;
 }
 

@@ -124,19 +124,10 @@ def random_script(cfg: dict, n_events: int, max_cycle: int, seed: int):
     return ev
 
 
-def load_trace(path: str, cfg: dict):
-    """Trace replay input (SURVEY 8(f) NEXT-f3; grammar of SPEC S:L533-534):
-    one record per line, `<node_linear_id> <hex_address> [R|W]`, `#` comments
-    and blank lines ignored.  Each node's records become its address stream in
-    file order: script events (0, node, tag) with tag = (address // line bytes)
-    mod TPN*N (reading R41), consumed one per generation opportunity in place
-    of the Philox draw (DESIGN 3.3; the paper feeds a trace per cycle, P:L233,
-    L276).  R/W is accepted and ignored (the model has no dirty state).
-    Returns the event list; raises ValueError on a malformed line."""
+def _trace_records(path: str, cfg: dict):
     N = cfg["mesh_w"] * cfg["mesh_h"]
     space = cfg["tags_per_node"] * N
     line_bytes = max(1, int(cfg.get("l2_line_bytes", 32)))
-    ev = []
     with open(path) as f:
         for ln, line in enumerate(f, 1):
             body = line.split("#", 1)[0].strip()
@@ -149,5 +140,31 @@ def load_trace(path: str, cfg: dict):
             addr = int(tok[1], 16)
             if not 0 <= node < N or addr < 0:
                 raise ValueError("%s:%d: node or address out of range" % (path, ln))
-            ev.append((0, node, (addr // line_bytes) % space))
-    return ev
+            yield (0, node, (addr // line_bytes) % space)
+
+
+def load_trace(path: str, cfg: dict):
+    """Trace replay input (SURVEY 8(f) NEXT-f3; grammar of SPEC S:L533-534):
+    one record per line, `<node_linear_id> <hex_address> [R|W]`, `#` comments
+    and blank lines ignored.  Each node's records become its address stream in
+    file order: script events (0, node, tag) with tag = (address // line bytes)
+    mod TPN*N (reading R41), consumed one per generation opportunity in place
+    of the Philox draw (DESIGN 3.3; the paper feeds a trace per cycle, P:L233,
+    L276).  R/W is accepted and ignored (the model has no dirty state).
+    Returns the event list; raises ValueError on a malformed line."""
+    return list(_trace_records(path, cfg))
+
+
+def trace_chunks(path: str, cfg: dict, records: int):
+    """The same trace read lazily in chunks of `records` records, for the
+    streamed replay (NocSim.push_script, DESIGN R57): only one chunk is held
+    in host memory, and pushed chunks are merged on the device as they are
+    needed.  Every record has cycle 0, so each node's queue stays in file order."""
+    chunk = []
+    for r in _trace_records(path, cfg):
+        chunk.append(r)
+        if len(chunk) == records:
+            yield chunk
+            chunk = []
+    if chunk:
+        yield chunk

@@ -5,6 +5,7 @@ hash (the model is integer and deterministic, DESIGN 3).
 All tests need a B200 (sm_100a).
 """
 import collections
+import os
 import random
 
 import pytest
@@ -601,3 +602,62 @@ def test_memory_nodes_c3_and_bands():
             g.run(k)
             o.run(k)
         assert_same(g, o)
+
+
+def _pieces(script, bounds):
+    out = [[] for _ in range(len(bounds) + 1)]
+    for e in script:
+        out[sum(1 for b in bounds if e[0] >= b)].append(e)
+    return out
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode", [W.MODE_UR, W.MODE_LSPD])
+def test_streamed_script_gpu(mode, engine):
+    """NEXT-f3 streamed trace replay (R57): a script pushed in pieces (some
+    before their events are due, merged before the run; some well ahead,
+    merged after it while their copy overlapped the run; one late, after its
+    events were due) -- bit-exact against the oracle fed the same pushes."""
+    if mode == W.MODE_UR:
+        cfg = W.make(mesh_w=24, mesh_h=20, mode=W.MODE_UR, thr_inj=0, sendq_cap=16)
+    else:
+        cfg = W.lspd(24, 20, thr_inj=0, sendq_cap=64, l2_sets=2, mem_lat=20)
+    script = W.random_script(cfg, 6000, 3000, seed=33)
+    parts = _pieces(script, [300, 900, 1000, 2200])
+    g = nb.NocSim(cfg, script=parts[0], engine=engine)
+    o = Oracle(cfg, script=parts[0])
+    plan = [(parts[1], 250), (parts[2], 640), (parts[3], 150), ([], 300), (parts[4], 2000)]
+    for piece, k in plan:
+        g.push_script(piece)
+        o.push_script(piece)
+        g.run(k)
+        o.run(k)
+    assert g.drain(100000) == o.drain(100000)
+    assert_same(g, o)
+
+
+def test_streamed_script_bands_and_trace_chunks():
+    """Pushed pieces on 3 virtual bands (each band keeps its nodes' events) and
+    a trace file streamed in chunks, against the oracle."""
+    cfg = W.lspd(40, 37, thr_inj=0, sendq_cap=64, l2_sets=4, mem_lat=30)
+    script = W.random_script(cfg, 20000, 4000, seed=4)
+    parts = _pieces(script, [1000, 2500])
+    for bands, engine in ((3, nb.ENGINE_TILED), (2, nb.ENGINE_PERSIST)):
+        g = nb.NocSim(cfg, script=parts[0], bands=bands, engine=engine)
+        o = Oracle(cfg, script=parts[0])
+        for piece, k in ((parts[1], 900), (parts[2], 1700), ([], 2000)):
+            g.push_script(piece)
+            o.push_script(piece)
+            g.run(k)
+            o.run(k)
+        assert_same(g, o)
+    cfg = W.c1b(thr_inj=0)
+    path = os.path.join(os.path.dirname(__file__), "golden", "trace_4x4.txt")
+    g = nb.NocSim(cfg)
+    o = Oracle(cfg)
+    for c in W.trace_chunks(path, cfg, 4):
+        g.push_script(c)
+        o.push_script(c)
+    g.run(3000)
+    o.run(3000)
+    assert_same(g, o)
