@@ -33,6 +33,8 @@ KERNELS = {1: "k_step", 2: "k_persist", 3: "k_tiled", 4: "k_tiled4"}
 UNIT = "node-cycles/s"
 WORKLOADS = {
     "c3": ("208x208 LSPD (BASELINE configs[2], paper's largest mesh)", W.c3),
+    "c1a": ("4x4 uniform random lambda 0.1 (BASELINE configs[0], C1a)", W.c1a),
+    "c1b": ("4x4 LSPD (BASELINE configs[0], C1b)", W.c1b),
     "c2": ("64x64 LSPD (BASELINE configs[1])", W.c2),
     "c4ur": ("208x208 uniform random lambda 0.3 (BASELINE configs[3])", lambda seed=1: W.c4(0.3, seed=seed)),
     "c5": ("1024x1024 LSPD (BASELINE configs[4])", W.c5),
@@ -250,7 +252,8 @@ def run_ours(args):
         try:
             tj = json.load(open(tf))
             traffic = tj.get("dram_bytes_per_launch")
-            ncu_info = {k: tj.get(k) for k in ("dram_bytes_per_node_cycle", "lts_bytes_per_node_cycle", "summary")}
+            ncu_info = {k: tj.get(k) for k in ("dram_bytes_per_node_cycle", "lts_bytes_per_node_cycle",
+                                              "warp_inst_per_node_cycle", "l2_hit_rate_pct", "summary")}
         except Exception:
             traffic = None
 

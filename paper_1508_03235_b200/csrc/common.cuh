@@ -257,6 +257,20 @@ __device__ __forceinline__ uint32_t defl_port(uint32_t freem, uint32_t route)
     return PW;
 }
 
+// Link flit arrays flit[parity]: input slot d of local node l.  Node-major
+// (the four slots of a node in one 64-byte block: a node's present flits share
+// sectors, and the per-cycle hot set is a quarter as spread) unless built with
+// NOC_FLIT_SLOT_MAJOR (the round-1 layout, d * nloc + l) for A/B.
+__host__ __device__ __forceinline__ size_t flit_at(uint32_t nloc, uint32_t d, uint32_t l)
+{
+#ifdef NOC_FLIT_SLOT_MAJOR
+    return (size_t)d * nloc + l;
+#else
+    (void)nloc;
+    return (size_t)l * 4u + d;
+#endif
+}
+
 constexpr uint32_t LL_EMPTY = 0xFFFFFFFFu;   // dst field all ones: never a node (N <= 2^21-1)
 
 __host__ __device__ __forceinline__ uint8_t stamp_of(uint64_t cycle) { return (uint8_t)(0x80u | (cycle & 0x7Fu)); }

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(PERSIST_BLOCK, PERSIST_MIN_BLOCKS) k_persist(c
             if (ln < hi_node) {
                 const uint32_t pb = (uint32_t)t & 1u;
 #pragma unroll
-                for (uint32_t d = 0; d < 4; ++d) prefetch_l1(&S.flit[pb][(size_t)d * S.nloc + ln]);
+                for (uint32_t d = 0; d < 4; ++d) prefetch_l1(&S.flit[pb][flit_at(S.nloc, d, ln)]);
             }
 #endif
 #ifdef NOC_AB_PF2
@@ -220,7 +220,7 @@ __device__ bool read_slot(const Dev &S, uint32_t l, uint32_t d, uint64_t t, Flit
     }
     uint32_t fl = S.flag[b][l];
     if (((fl >> (8u * d)) & 0xFFu) != stamp_of(t)) return false;
-    uint4 v = S.flit[b][(size_t)d * S.nloc + l];
+    uint4 v = S.flit[b][flit_at(S.nloc, d, l)];
     f = Flit{v.x, v.y, v.z, v.w};
     return true;
 }

@@ -1148,7 +1148,7 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
     NodeCtx c;
     c.l = l;
     c.n = S.n0 + l;
-    c.y = c.n / S.W;
+    c.y = __umulhi(c.n, S.wmagic);   // n / W (exact for n < 2^21)
     c.x = c.n - c.y * S.W;
     c.deg = (c.y > 0) + (c.y + 1 < S.H) + (c.x + 1 < S.W) + (c.x > 0);
     c.qctl = S.fifo_ctl[l];
@@ -1174,7 +1174,7 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
 #pragma unroll
     for (uint32_t d = 0; d < 4; ++d) {
         if (((fl >> (8u * d)) & 0xFFu) == st) {
-            uint4 v = __ldcg(&S.flit[b][(size_t)d * S.nloc + l]);
+            uint4 v = __ldcg(&S.flit[b][flit_at(S.nloc, d, l)]);
             in.f[d] = Flit{v.x, v.y, v.z, v.w};
             in.present |= 1u << d;
         }
@@ -1205,7 +1205,7 @@ __device__ __forceinline__ bool node_step_global(const Dev &S, const Sink &K, ui
             case PE: m = l + 1u; slot = PW; break;
             default: m = l - 1u; slot = PE; break;
             }
-            fl[(size_t)slot * nl + m] = make_uint4(f.x, f.y, f.z, f.w);
+            fl[flit_at(nl, slot, m)] = make_uint4(f.x, f.y, f.z, f.w);
             reinterpret_cast<uint8_t *>(fg)[(size_t)m * 4u + slot] = st1;
         });
         c.busy_flit = nf > (has_ej ? 1u : 0u);

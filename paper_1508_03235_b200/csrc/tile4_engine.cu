@@ -193,7 +193,7 @@ k_tiled4(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t 
         bool has = false;
         const uint32_t si = (b0 * 4u + g) * np + i;
         if (my_int && ((S.flag[b0][c.l] >> (8u * g)) & 0xFFu) == stamp_of(t0)) {
-            sflit[si] = S.flit[b0][(size_t)g * S.nloc + c.l];
+            sflit[si] = S.flit[b0][flit_at(S.nloc, g, c.l)];
             has = true;
         }
         sst[si] = has ? (uint32_t)t0 : (uint32_t)t0 - 1u;
@@ -418,7 +418,7 @@ k_tiled4(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t 
         const uint32_t si = (be * 4u + g) * np + i;
         uint8_t fb = 0;
         if (my_int && sst[si] == (uint32_t)tend) {
-            S.flit[be][(size_t)g * S.nloc + c.l] = sflit[si];
+            S.flit[be][flit_at(S.nloc, g, c.l)] = sflit[si];
             fb = stamp_of(tend);
         }
         reinterpret_cast<uint8_t *>(&S.flag[be][c.l])[g] = fb;

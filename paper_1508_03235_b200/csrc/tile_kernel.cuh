@@ -402,7 +402,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
             if (((intl >> d) & 1u) && ((fl >> (8u * d)) & 0xFFu) == s0) {
-                sflit[(b0 * 4u + d) * np + i] = S.flit[b0][(size_t)d * S.nloc + c.l];
+                sflit[(b0 * 4u + d) * np + i] = S.flit[b0][flit_at(S.nloc, d, c.l)];
                 occ |= 1u << (8u * d);
             }
         }
@@ -801,7 +801,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             if (((intl >> d) & 1u) && ((occ >> (8u * d)) & 0xFFu)) {
                 const uint4 v = sflit[(be * 4u + d) * np + i];
                 if ((uint32_t)tend - v.z > LIFE_MAX) errf |= ERR_AGE;   // R32
-                S.flit[be][(size_t)d * S.nloc + c.l] = v;
+                S.flit[be][flit_at(S.nloc, d, c.l)] = v;
                 gfl |= (uint32_t)ste << (8u * d);
             }
         }

@@ -61,7 +61,11 @@ lines += ["", "# top source lines by stall samples (% stall, % instructions exec
 for k, v in sorted(res.items(), key=lambda x: -x[1][1])[:20]:
     lines.append("%5.1f%% stall %5.1f%% instr  %s:%d  %s" % (100 * v[1] / ts, 100 * v[0] / ti, k[0], k[1], v[2]))
 open(out, "w").write("\n".join(lines) + "\n")
+inst = float(d['smsp__inst_executed.sum'].replace(',', '')) if 'smsp__inst_executed.sum' in d else 0.0
+l2hit = float(d['lts__t_sector_hit_rate.pct'].replace(',', '')) if 'lts__t_sector_hit_rate.pct' in d else None
 json.dump({"kernel": title, "dram_bytes_per_launch": dram, "lts_bytes_per_launch": lts, "cycles_per_launch": cycles,
            "nodes": nodes, "dram_bytes_per_node_cycle": dram / cycles / nodes,
-           "lts_bytes_per_node_cycle": lts / cycles / nodes, "summary": out}, open(traffic, "w"), indent=1)
+           "lts_bytes_per_node_cycle": lts / cycles / nodes,
+           "warp_inst_per_node_cycle": inst / cycles / nodes, "l2_hit_rate_pct": l2hit,
+           "summary": out}, open(traffic, "w"), indent=1)
 print(open(out).read())
