@@ -243,7 +243,7 @@ def run_ours(args):
     launches = info1["kernel_launches"] - info0["kernel_launches"]
     # the TILED engines also launch the LL-slot refresh kernel before each
     # node-step launch (one per band of this process)
-    gpu_launches = launches * (2 if info1["engine"] in (3, 4) else 1)
+    gpu_launches = launches * (2 if info1["engine"] in (3, 4) and not info1.get("cluster") else 1)
     per_launch_ms = dev_ms / max(launches, 1)
     achieved = B * nodecycles / (dev_ms / 1e3) / 1e9          # per GPU (this rank's nodes)
     traffic, ncu_info = None, None

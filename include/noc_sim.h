@@ -203,7 +203,10 @@ typedef struct noc_sim_info {
     uint64_t kernel_launches;  /* node-step launches issued so far                 */
     uint64_t cycles_run;       /* cycles advanced so far                           */
     int32_t  sm_count;
-    int32_t  reserved[7];
+    uint32_t cluster;          /* TILED: > 0 = the band runs as one thread-block
+                                  cluster of this many tiles (DSMEM links, no
+                                  LL slots, no refresh launches)              */
+    int32_t  reserved[6];
 } noc_sim_info;
 
 typedef struct noc_sim noc_sim;

@@ -69,7 +69,7 @@ class noc_sim_info(C.Structure):
         ("nodes_local", C.c_uint32), ("row0", C.c_uint32), ("rows", C.c_uint32),
         ("device_bytes", C.c_uint64), ("loc_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("cycles_run", C.c_uint64),
-        ("sm_count", C.c_int32), ("reserved", C.c_int32 * 7),
+        ("sm_count", C.c_int32), ("cluster", C.c_uint32), ("reserved", C.c_int32 * 6),
     ]
 
 

@@ -19,6 +19,7 @@ struct DevSet {
     uint32_t nbands;
     uint32_t tile0[MAX_BANDS + 1];   // first CTA of each band
     uint32_t general;                // several bands or ranks: band lookup and system-scope band-edge links
+    uint32_t cluster;                // TILED cluster exchange: the tiles form one cluster (FEAT bit 3)
 };
 
 // TILED engine (tile_engine.cu): tiled_plan picks the tiling of one band
@@ -31,6 +32,9 @@ uint32_t tiled_kernel_mode(const Dev &D);
 cudaError_t launch_script_count(const Dev &S, const uint32_t *add_off, uint32_t *cnt, cudaStream_t st);
 cudaError_t launch_script_merge(const Dev &S, const uint32_t *add_off, const uint4 *add_ev, const uint32_t *new_off,
                                 uint4 *new_ev, uint32_t *new_base, cudaStream_t st);
+// the cluster exchange: one band of <= TILE_CLUSTER_MAX tiles as one cluster
+constexpr uint32_t TILE_CLUSTER_MAX = 16;
+cudaError_t tiled_prepare_cluster(uint32_t mode, uint32_t nb, uint32_t np, uint32_t tiles, uint32_t *smem_hist);
 cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t np, uint32_t total_tiles, int device,
                           uint32_t *smem_hist);
 cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t tpad, uint32_t smem_hist,

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -492,7 +493,33 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
     // AUTO tries TILED (one thread per node), then TILED4 (4 lanes per node,
     // 2 CTAs per SM), then PERSIST: TILED is the fastest at the bench size
     // (DESIGN 6.4, profiles/r01_ab_engines.txt)
+    // opt-in (NOCSIM_CLUSTER=1): a single band of up to TILE_CLUSTER_MAX tiles
+    // runs as ONE thread-block cluster -- cross-tile links are DSMEM stores and
+    // the cycle barrier is the cluster barrier (tile_kernel.cuh, FEAT bit 3).
+    // Parity-green, but not the default: at C2 it is faster only without load
+    // (1.01 vs 1.79 us per cycle idle, 4.2 vs 3.2 at lambda 0.05: 16 CTAs of 256
+    // nodes wait for the slowest of 128 warps every cycle, profiles/r02_cluster_c2.txt)
+    if ((s->engine == NOC_ENGINE_AUTO || s->engine == NOC_ENGINE_TILED) && s->nb == 1 && s->world == 1 &&
+        cfg->route == 0 && cfg->inject_mode == 0 && getenv("NOCSIM_CLUSTER")) {
+        const uint64_t nodes = (uint64_t)s->D[0].W * s->D[0].rows;
+        uint32_t tiles = 0, np = 0;
+        if (nodes > TILE_BLOCK_MAX && nodes <= (uint64_t)TILE_CLUSTER_MAX * TILE_BLOCK_MAX &&
+            tiled_plan(s->D[0], TILE_CLUSTER_MAX, &tiles, &np) && tiles > 1 &&
+            tiled_prepare_cluster(tiled_kernel_mode(s->D[0]), cfg->hist_bins, np, tiles, &s->t_smem_hist) ==
+                cudaSuccess) {
+            s->engine = NOC_ENGINE_TILED;
+            s->t_tpad = np;
+            s->set.nbands = 1;
+            s->set.general = 0;
+            s->set.cluster = tiles;
+            s->set.tile0[0] = 0;
+            s->set.tile0[1] = tiles;
+            s->set.d[0] = s->D[0];
+        }
+        cudaGetLastError();
+    }
     for (uint32_t cand : {NOC_ENGINE_TILED, NOC_ENGINE_TILED4}) {
+        if (s->set.cluster) break;
         if (!(s->engine == NOC_ENGINE_AUTO || s->engine == cand)) continue;
         if (cand == NOC_ENGINE_TILED4 && cfg->inject_mode) continue;   // four lanes per router (R43)
         const bool four = cand == NOC_ENGINE_TILED4;
@@ -525,7 +552,7 @@ extern "C" int noc_sim_create(const noc_sim_config *cfg, noc_sim **out)
             return bail(fail(NOC_EINVAL, std::string("TILED engine does not fit this mesh: ") + cudaGetErrorString(ce)));
     }
     if (s->engine == NOC_ENGINE_AUTO) s->engine = NOC_ENGINE_PERSIST;
-    if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) {
+    if ((s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) && !s->set.cluster) {
         for (int k = 0; k < s->nb; ++k)
             if ((rc = dalloc(s, &s->D[k].ll, (size_t)32u * s->D[k].nloc))) return bail(rc);
         // neighbour bands' boundary slots
@@ -755,7 +782,8 @@ static int advance_launches(noc_sim *s, uint64_t n, uint32_t *activity)
         uint64_t done = 0;
         while (done < n) {
             uint32_t k = (uint32_t)std::min<uint64_t>(n - done, PERSIST_CHUNK);
-            for (int b = 0; b < s->nb; ++b) CU(launch_ll_refresh(s->D[b], s->t + done, s->stream));
+            if (!s->set.cluster)
+                for (int b = 0; b < s->nb; ++b) CU(launch_ll_refresh(s->D[b], s->t + done, s->stream));
             // ranks: every rank's refresh completes before any rank's kernel
             // starts, else a fast neighbour's first boundary stores (stamp t0+1)
             // could be re-stamped t0-1 by this rank's late refresh (a stream-
@@ -942,7 +970,7 @@ extern "C" int noc_sim_drain(noc_sim *s, uint64_t max_cycles, uint64_t *used, in
             s->t = t0 + k;
             // boundary slots were stamped up to the end of the chunk: re-stamp
             // them EMPTY for the rewound cycle (nothing is in flight)
-            if (s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4)
+            if ((s->engine == NOC_ENGINE_TILED || s->engine == NOC_ENGINE_TILED4) && !s->set.cluster)
                 for (int b = 0; b < s->nb; ++b) CU(launch_ll_reset(s->D[b], s->t, s->stream));
             if ((rc = allreduce_u32(s, s->d_scratch + DRAIN_CHUNK, 1))) return rc;
         } else {
@@ -1054,6 +1082,7 @@ extern "C" int noc_sim_get_info(noc_sim *s, noc_sim_info *o)
     o->device_bytes = s->bytes;
     o->loc_bytes = s->loc_bytes;
     o->kernel_launches = s->launches;
+    o->cluster = s->set.cluster;
     o->cycles_run = s->t;
     o->sm_count = s->sm_count;
     o->reserved[2] = s->P;

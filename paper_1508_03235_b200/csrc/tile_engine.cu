@@ -27,7 +27,9 @@ __global__ void k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t 
     extern template __global__ void k_tiled<M, false, 6>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *); \
     extern template __global__ void k_tiled<M, true, 6>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *);  \
     extern template __global__ void k_tiled<M, false, 7>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *); \
-    extern template __global__ void k_tiled<M, true, 7>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *);
+    extern template __global__ void k_tiled<M, true, 7>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *);  \
+    extern template __global__ void k_tiled<M, false, 8>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *); \
+    extern template __global__ void k_tiled<M, true, 8>(const __grid_constant__ DevSet, uint64_t, uint32_t, uint32_t, uint32_t *);
 NOC_TILED_EXTERN(0)
 NOC_TILED_EXTERN(1)
 NOC_TILED_EXTERN(2)
@@ -126,7 +128,7 @@ static const void *tiled_fn(uint32_t mode, bool drain, uint32_t feat)
 #define NOC_TD(M, F) (drain ? (const void *)k_tiled<M, true, F> : (const void *)k_tiled<M, false, F>)
 #define NOC_TF4(M, B) (feat == 3u + B ? NOC_TD(M, 3 + B) : feat == 2u + B ? NOC_TD(M, 2 + B) : \
                        feat == 1u + B ? NOC_TD(M, 1 + B) : NOC_TD(M, 0 + B))
-#define NOC_TF(M) (feat >= 4u ? NOC_TF4(M, 4) : NOC_TF4(M, 0))
+#define NOC_TF(M) (feat == 8u ? NOC_TD(M, 8) : feat >= 4u ? NOC_TF4(M, 4) : NOC_TF4(M, 0))
     return mode == 2u ? NOC_TF(2) : mode == 1u ? NOC_TF(1) : NOC_TF(0);
 #undef NOC_TF
 #undef NOC_TF4
@@ -164,6 +166,40 @@ cudaError_t tiled_prepare(uint32_t mode, uint32_t route, uint32_t nb, uint32_t n
     return cudaSuccess;
 }
 
+// Cluster exchange (FEAT 8): one band of tiles <= TILE_CLUSTER_MAX launched as
+// a single thread-block cluster (co-resident by construction)
+cudaError_t tiled_prepare_cluster(uint32_t mode, uint32_t nb, uint32_t np, uint32_t tiles, uint32_t *smem_hist)
+{
+    if (tiles < 2 || tiles > TILE_CLUSTER_MAX) return cudaErrorInvalidConfiguration;
+    Dev tmp;
+    tmp.nb = nb;
+    size_t smem = tiled_smem_bytes(tmp, np, true);
+    *smem_hist = 1u;
+    for (int drain = 0; drain < 2; ++drain) {
+        const void *fn = tiled_fn(mode, drain != 0, 8u);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = tiles;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(tiles);
+        cfg.blockDim = dim3(np);
+        cfg.dynamicSmemBytes = smem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+        if (e != cudaSuccess) return e;
+        if (nclusters < 1) return cudaErrorCooperativeLaunchTooLarge;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_ll_refresh(const Dev &S, uint64_t t0, cudaStream_t st)
 {
     k_ll_refresh<<<256, 256, 0, st>>>(S, t0);
@@ -177,12 +213,27 @@ cudaError_t launch_tiled(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t t
     void *args[] = {(void *)&P, (void *)&t0, (void *)&ncyc, (void *)&smem_hist, (void *)&activity};
     const bool dr = activity != nullptr;
     const void *fn = tiled_fn(tiled_kernel_mode(P.d[0]), dr,
-                              P.d[0].route | (P.d[0].inject_mode ? 2u : 0u) | (P.general ? 4u : 0u));
+                              P.cluster ? 8u : P.d[0].route | (P.d[0].inject_mode ? 2u : 0u) | (P.general ? 4u : 0u));
     // the dynamic shared-memory limit is a per-function (process-wide)
     // attribute: another handle of a different size may have lowered it
     {
         const cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) return ea;
+    }
+    if (P.cluster) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = P.cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(P.cluster);
+        cfg.blockDim = dim3(tpad);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelExC(&cfg, fn, args);
     }
     return cudaLaunchCooperativeKernel(fn, dim3(P.tile0[P.nbands]), dim3(tpad), args, smem, st);
 }

@@ -237,6 +237,31 @@ __device__ __forceinline__ void sts8_if(bool c, uint32_t a)
                  ::"r"((uint32_t)c), "r"(a), "r"(1u) : "memory");
 }
 
+// Cluster exchange (FEAT bit 3): the whole band is ONE thread-block cluster of
+// <= 16 tiles; a link to another tile is a store into that CTA's shared-memory
+// slot (DSMEM, st.shared::cluster at the address mapa gives), and the cycle
+// barrier is the cluster barrier (arrive.release / wait.acquire), which orders
+// those stores before the next cycle's latch: no boundary polling at all.
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t a, const Flit &v)
+{
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cluster_u8(uint32_t a)
+{
+    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "r"(1u) : "memory");
+}
+__device__ __forceinline__ void cluster_barrier()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // First choice of a flit with destination dst at node (n, x, y): eject at the
 // destination, else the x-port while dx != 0, else the y-port (PMDR).
 // Written as predicated selects (the nested ternary compiled to a branch
@@ -289,6 +314,7 @@ __global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
 {
     constexpr uint32_t FULL = 0xFFFFFFFFu;
+    constexpr bool CL = (FEAT & 8u) != 0u;   // cluster exchange (one band, <= 16 tiles)
     // this CTA's band and tile
     // FEAT bit 2: several bands in this launch (virtual bands).  With one band
     // the parameters are read at constant offsets (constant-bank operands of
@@ -376,7 +402,23 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             }
             if ((intl >> d) & 1u) na[d] = (((d ^ 1u) * np + mi) * 16u) | ((mi * 4u + (d ^ 1u)) << 16);
             sna[d * np + i] = na[d];
-            if ((ext >> d) & 1u) {
+            if (CL && ((ext >> d) & 1u)) {
+                // the receiver's tile (= cluster rank) and its slot there
+                const uint32_t vx = c.x + (d == PE ? 1u : 0u) - (d == PW ? 1u : 0u);
+                const uint32_t vy = c.y + (d == PS ? 1u : 0u) - (d == PN ? 1u : 0u);
+                const uint32_t rb = tile_of(vy - S.row0, S.rows, S.TY) * S.TX + tile_of(vx, S.W, S.TX);
+                const TileShape R = tile_shape(S, rb);
+                const uint32_t mr = tile_slot(R, vx - R.x0, vy - R.y0);
+                ExtIn e;
+                e.port = d;
+                e.inw = rb;
+                e.outw = (((d ^ 1u) * np + mr) * 16u) | ((mr * 4u + (d ^ 1u)) << 16);
+                e.sys = false;
+#pragma unroll
+                for (uint32_t j = 0; j < 4; ++j)
+                    if (j == nex) ex[j] = e;
+                ++nex;
+            } else if ((ext >> d) & 1u) {
                 ExtIn e;
                 e.port = d;
                 e.inw = (uint32_t)ll_index(S, 0, d, c.l, 0);
@@ -401,7 +443,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         uint32_t occ = 0;
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
-            if (((intl >> d) & 1u) && ((fl >> (8u * d)) & 0xFFu) == s0) {
+            if ((((CL ? exist : intl) >> d) & 1u) && ((fl >> (8u * d)) & 0xFFu) == s0) {
                 sflit[(b0 * 4u + d) * np + i] = S.flit[b0][flit_at(S.nloc, d, c.l)];
                 occ |= 1u << (8u * d);
             }
@@ -480,7 +522,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     // latency overlaps the rest of cycle t (Phase 3, Phase 1 of t+1, the
     // barrier).  Phase 1 of the first cycle runs in the prologue.
     unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0w = 0, b1w = 0, b2w = 0, b3w = 0;
-    if (active && ext) {
+    if (!CL && active && ext) {
         const unsigned long long *const llp = S.ll + (size_t)b0 * pstride;
         ll_load2(e0.sys, llp + e0.inw, a0, a1);
         ll_load2(e0.sys, llp + e0.inw + 2, a2, a3);
@@ -495,7 +537,9 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         else phase1_lspd_win<MODE == 2u>(S, K, c, t0, wbase, wmask);
         if (windows) wake = wake_from((uint32_t)t0);
     }
-    __syncthreads();
+    // cluster exchange: every CTA's slots are initialised before any remote store
+    if (CL) cluster_barrier();
+    else __syncthreads();
 
     for (uint32_t cc = 0; cc < ncyc; ++cc) {
         const uint64_t t = t0 + cc;
@@ -519,7 +563,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             // (word 0 carries stamp t and, for a flit rather than EMPTY, so do
             // words 1..3); a flit is parked in the node's own shared slot so
             // all four link inputs are latched alike below
-            if (ext) {
+            if (!CL && ext) {
                 bool w0 = true, w1 = e1.port != NOPORT, w2 = ex[2].port != NOPORT, w3 = ex[3].port != NOPORT;
                 uint32_t spins = 0;
                 while (true) {
@@ -698,7 +742,19 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
             // critical path of the neighbouring tiles.  A routed flit, else an
             // explicit EMPTY, on every boundary port every cycle.  Then the
             // polls of the next cycle's boundary inputs.
-            if (ext) {
+            if (CL && ext) {
+                // cluster exchange: a routed flit goes straight into the
+                // receiving CTA's slot of cycle t+1 (no EMPTY words needed)
+#pragma unroll
+                for (uint32_t j = 0; j < 4; ++j) {
+                    const ExtIn &e = ex[j];
+                    if (e.port == NOPORT || !((used >> e.port) & 1u)) continue;
+                    const Flit g = pick5(f, (inv >> (4u * e.port)) & 15u);
+                    if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32, at a cross-tile hop
+                    st_cluster_v4(mapa_rank(fa + nb1 * FSTR + (e.outw & 0xFFFFu), e.inw), g);
+                    st_cluster_u8(mapa_rank(oa + nb1 * OSTR + (e.outw >> 16), e.inw));
+                }
+            } else if (ext) {
 #pragma unroll
                 for (uint32_t j = 0; j < 4; ++j) {
                     const ExtIn &e = ex[j];
@@ -779,7 +835,8 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         // The cycle barrier is a full BAR.SYNC: it orders this cycle's shared-
         // memory link stores before the next cycle's loads.
         if (DRAIN && busy) s_busy[cc & 1u] = cc + 1u;
-        __syncthreads();
+        if (CL) cluster_barrier();
+        else __syncthreads();
         if (DRAIN && i == 0 && s_busy[cc & 1u] == cc + 1u) atomicAdd(&activity[cc], 1u);
         if (s_abort) break;
     }
@@ -798,7 +855,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         uint32_t gfl = 0;
 #pragma unroll
         for (uint32_t d = 0; d < 4; ++d) {
-            if (((intl >> d) & 1u) && ((occ >> (8u * d)) & 0xFFu)) {
+            if ((((CL ? exist : intl) >> d) & 1u) && ((occ >> (8u * d)) & 0xFFu)) {
                 const uint4 v = sflit[(be * 4u + d) * np + i];
                 if ((uint32_t)tend - v.z > LIFE_MAX) errf |= ERR_AGE;   // R32
                 S.flit[be][flit_at(S.nloc, d, c.l)] = v;

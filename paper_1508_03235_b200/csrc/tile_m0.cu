@@ -10,5 +10,6 @@ NOC_TILED_INST(false, 0) NOC_TILED_INST(true, 0) NOC_TILED_INST(false, 1) NOC_TI
 NOC_TILED_INST(false, 2) NOC_TILED_INST(true, 2) NOC_TILED_INST(false, 3) NOC_TILED_INST(true, 3)
 NOC_TILED_INST(false, 4) NOC_TILED_INST(true, 4) NOC_TILED_INST(false, 5) NOC_TILED_INST(true, 5)
 NOC_TILED_INST(false, 6) NOC_TILED_INST(true, 6) NOC_TILED_INST(false, 7) NOC_TILED_INST(true, 7)
+NOC_TILED_INST(false, 8) NOC_TILED_INST(true, 8)   // cluster exchange
 #undef NOC_TILED_INST
 }  // namespace noc

@@ -661,3 +661,16 @@ def test_streamed_script_bands_and_trace_chunks():
     g.run(3000)
     o.run(3000)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("cfg", [W.c2(), W.make(mesh_w=40, mesh_h=30, mode=W.MODE_UR, lam=0.2),
+                                 W.lspd(31, 29, lam=0.2, l1_sets=2, l1_ways=2), W.c2(mem_mode=W.MEM_HOME)],
+                         ids=["c2", "ur40x30", "lspd31x29_l1", "c2_memhome"])
+def test_cluster_exchange(cfg, monkeypatch):
+    """The opt-in cluster exchange of the TILED engine (NOCSIM_CLUSTER=1: the
+    band as one thread-block cluster, DSMEM links, cluster barrier), across
+    launch boundaries and a drain, bit-exact against the oracle."""
+    monkeypatch.setenv("NOCSIM_CLUSTER", "1")
+    g, o = both(cfg, 2600, nb.ENGINE_TILED, split=[1, 600, 1999], drain=100000)
+    assert g.info()["cluster"] > 1
+    assert_same(g, o)
