@@ -7,4 +7,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout ${1:-2400} python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gputest.log 2>&1
 echo "rc=$?" >> gpurun_out/gputest.log
 tail -40 gpurun_out/gputest.log
-tail -3 gpurun_out/bench.log gpurun_out/smoke.log
+tail -n 3 gpurun_out/bench.log gpurun_out/smoke.log
