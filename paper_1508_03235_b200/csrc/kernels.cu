@@ -42,9 +42,6 @@ __device__ __forceinline__ void flush_acc(const Dev &S, const Acc &a, unsigned i
     }
 }
 
-// ------------------------------------------------------------------ init
-__global__ void k_init_loc_nop() {}
-
 // ------------------------------------------------------------------ STEP engine
 template <uint32_t MODE>
 __global__ void __launch_bounds__(256) k_step(Dev S, uint64_t t, uint32_t *activity)
