@@ -226,6 +226,11 @@ uint32_t noc_sim_abi_version(void);
  * this and broadcasts it).  Errors: NOC_ENCCL. */
 int noc_sim_nccl_unique_id(uint8_t out[128]);
 
+/* The rows [*row0, *row0 + *rows) of band `rank` of `world_size` on a mesh of
+ * mesh_h rows: row0 = floor(rank * mesh_h / world_size) (the partition every
+ * handle uses; host only, no device needed).  Errors: NOC_EINVAL. */
+int noc_sim_band_rows(uint32_t mesh_h, int32_t world_size, int32_t rank, uint32_t *row0, uint32_t *rows);
+
 /* Create a simulation at cycle 0 ("initialize" kernel): all links and
  * FIFOs empty, cores IDLE, L2 lines invalid, directory empty, counters 0.
  * cfg is copied (including the script).  When world_size > 1 this call is

@@ -96,6 +96,7 @@ def lib():
         L.noc_sim_run_timed.argtypes = [P, C.c_uint64, C.POINTER(C.c_double)]
         L.noc_sim_drain.argtypes = [P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
         L.noc_sim_push_script.argtypes = [P, C.POINTER(noc_sim_event), C.c_uint64]
+        L.noc_sim_band_rows.argtypes = [C.c_uint32, C.c_int32, C.c_int32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.noc_sim_stats.argtypes = [P, C.POINTER(noc_sim_counters), P, P, P, C.c_uint32]
         L.noc_sim_state_hash.argtypes = [P, C.POINTER(C.c_uint64)]
         L.noc_sim_get_info.argtypes = [P, C.POINTER(noc_sim_info)]

@@ -236,6 +236,15 @@ static void band_rows(uint32_t H, int P, int g, uint32_t *row0, uint32_t *rows)
     *rows = b - a;
 }
 
+extern "C" int noc_sim_band_rows(uint32_t mesh_h, int32_t world_size, int32_t rank, uint32_t *row0, uint32_t *rows)
+{
+    if (!row0 || !rows) return fail(NOC_EINVAL, "null argument");
+    if (world_size < 1 || rank < 0 || rank >= world_size || (uint32_t)world_size > mesh_h)
+        return fail(NOC_EINVAL, "bad world_size/rank");
+    band_rows(mesh_h, world_size, rank, row0, rows);
+    return NOC_OK;
+}
+
 // allocate and initialise the state of one band (DESIGN 6.1)
 static int make_band(noc_sim *s, const noc_sim_config *cfg, int g, Dev &D)
 {

@@ -19,10 +19,13 @@ def env():
 
 
 def band_rows(mesh_h: int, world: int, rank: int):
-    """Rows [row0, row0+rows) of band `rank` of `world` (as the library splits)."""
-    a = rank * mesh_h // world
-    b = (rank + 1) * mesh_h // world
-    return a, b - a
+    """Rows [row0, row0+rows) of band `rank` of `world`: the library's own
+    partition (noc_sim_band_rows; host only)."""
+    import ctypes as C
+    import paper_1508_03235_b200 as pkg
+    a, n = C.c_uint32(), C.c_uint32()
+    pkg._check(pkg.lib().noc_sim_band_rows(mesh_h, world, rank, C.byref(a), C.byref(n)))
+    return a.value, n.value
 
 
 def share_nccl_id(make_id, group=None) -> bytes:

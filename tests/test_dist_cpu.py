@@ -23,8 +23,8 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1508_03235_b200 as pkg
     nid = pdist.share_nccl_id(pkg.noc_sim_nccl_unique_id)
-    rows = [pdist.band_rows(208, world, r) for r in range(world)]
-    out[rank] = (nid, rows)
+    # each rank asks the library for its own band
+    out[rank] = (nid, pdist.band_rows(208, world, rank))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -43,13 +43,17 @@ def test_two_ranks_share_nccl_id_and_bands(world):
         assert p.exitcode == 0
     ids = {bytes(out[r][0]) for r in range(world)}
     assert len(ids) == 1 and len(next(iter(ids))) == 128 and any(next(iter(ids)))
-    rows = out[0][1]
+    rows = [out[r][1] for r in range(world)]
     assert rows[0][0] == 0 and sum(r for _, r in rows) == 208
     assert all(rows[i][0] + rows[i][1] == rows[i + 1][0] for i in range(world - 1))
 
 
 def test_band_rows_partition():
+    """The library's partition (noc_sim_band_rows) is a contiguous cover of
+    the rows with band g starting at floor(g*H/P) (DESIGN 8)."""
     for h in (2, 7, 208, 1024):
         for w in range(1, min(h, 8) + 1):
             rows = [pdist.band_rows(h, w, r) for r in range(w)]
-            assert rows[0][0] == 0 and sum(r for _, r in rows) == h and min(r for _, r in rows) >= 1
+            assert [a for a, _ in rows] == [g * h // w for g in range(w)]
+            assert sum(r for _, r in rows) == h and min(r for _, r in rows) >= 1
+            assert all(rows[i][0] + rows[i][1] == rows[i + 1][0] for i in range(w - 1))
