@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("NOCSIM_LIB") or os.path.join(HERE, "libnocsim.so")
-SOURCES = ["kernels.cu", "tile_engine.cu", "tile_m0.cu", "tile_m1.cu", "tile_m2.cu", "tile4_engine.cu", "runtime.cu"]
-HEADERS = ["common.cuh", "node_logic.cuh", "kernels.h", "tile_kernel.cuh"]
+SOURCES = ["kernels.cu", "persist_lean.cu", "tile_engine.cu", "tile_m0.cu", "tile_m1.cu", "tile_m2.cu", "tile4_engine.cu", "runtime.cu"]
+HEADERS = ["common.cuh", "node_logic.cuh", "kernels.h", "tile_kernel.cuh", "persist_kernel.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

@@ -7,7 +7,10 @@ namespace noc {
 constexpr uint32_t PERSIST_BLOCK = 256;
 // 3 co-resident PERSIST CTAs per SM (<= 80 registers): large meshes are DRAM-latency
 // bound and need the warps (A/B at C5: 24 vs 16 warps per SM, -18% per cycle)
-constexpr uint32_t PERSIST_MIN_BLOCKS = 3;
+#ifndef NOC_PERSIST_MIN_BLOCKS
+#define NOC_PERSIST_MIN_BLOCKS 3   // A/B builds: -DNOC_PERSIST_MIN_BLOCKS=N
+#endif
+constexpr uint32_t PERSIST_MIN_BLOCKS = NOC_PERSIST_MIN_BLOCKS;
 constexpr uint32_t TILE_BLOCK_MAX = 320;                  // nodes (= threads) per CTA: C3 tiles are 300; 320 leaves 204 registers (A/B: -2.7 % per cycle vs 512)
 constexpr uint32_t TILE_MIN_BLOCKS = 1;                   // co-resident CTAs per SM
 
@@ -52,6 +55,8 @@ cudaError_t launch_tiled4(const DevSet &P, uint64_t t0, uint32_t ncyc, uint32_t 
                           uint32_t *activity, cudaStream_t st);
 cudaError_t launch_ll_reset(const Dev &S, uint64_t t, cudaStream_t st);
 
+// lean PERSIST kernel (persist_lean.cu) for traffic mode 0 / 1
+const void *persist_fn_lean(uint32_t mode);
 cudaError_t launch_step(const Dev &S, uint64_t t, uint32_t *activity, cudaStream_t st);
 cudaError_t persist_configure(const Dev &S, int device, uint32_t nbands, uint32_t *grid, uint32_t *nodes_per_cta,
                               uint32_t *smem_hist);

@@ -117,7 +117,14 @@ static int dalloc(noc_sim *s, T **p, size_t count)
     void *q = nullptr;
     cudaError_t e = cudaMalloc(&q, b);
     if (e != cudaSuccess) return fail(NOC_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    // the zeroing runs on the legacy default stream, which the library's
+    // non-blocking streams are not ordered against: it must be complete
+    // before the buffer is filled by a copy or kernel on those streams (a
+    // late memset zeroed a merged script's offsets, losing a pushed piece).
+    // Waits for this memset only; running kernels on the library's streams
+    // are not waited for.
     e = cudaMemset(q, 0, b);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) return fail(NOC_ECUDA, std::string("cudaMemset: ") + cudaGetErrorString(e));
     s->allocs.push_back(q);
     s->alloc_bytes.push_back(b);

@@ -262,6 +262,24 @@ __device__ __forceinline__ void cluster_barrier()
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Split cycle barrier (DESIGN 6.3): one shared-memory mbarrier, one arrival
+// per warp per cycle (lane 0, after __syncwarp), release / acquire at CTA
+// scope; try_wait sleeps the warp in hardware until the phase completes.
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a)
+{
+    asm volatile("{\n\t.reg .b64 tok;\n\tmbarrier.arrive.release.cta.shared::cta.b64 tok, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+
 // First choice of a flit with destination dst at node (n, x, y): eject at the
 // destination, else the x-port while dx != 0, else the y-port (PMDR).
 // Written as predicated selects (the nested ternary compiled to a branch
@@ -334,6 +352,24 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     unsigned int *shist = smem_hist ? scnt + NCOUNTERS : nullptr;
     __shared__ int s_abort;
     __shared__ uint32_t s_busy[2];
+    // split cycle barrier (DESIGN 6.3), UR traffic only: there every warp has
+    // routing-heavy cycles and a Phase 1 draw after the publish, which the
+    // split lets overlap the other warps' routing (saturated 208x208 UR
+    // -6 %); with LSPD's rare, heavy-tailed services it measured 3 % slower
+    // than BAR.SYNC in the bench window (profiles/r02_ab_split_barrier.txt).
+    // Not in drain launches (they reduce a busy flag over the whole cycle)
+    // nor with the cluster exchange.
+#ifdef NOC_NO_SPLIT_BAR
+    constexpr bool SPLIT = false;
+#else
+    constexpr bool SPLIT = !DRAIN && !CL && MODE == 0u;
+#endif
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+    // a one-warp tile or a single-tile mesh keeps BAR.SYNC: without boundary
+    // waits to overlap, the mbarrier round trip only costs (4x4: +9 %,
+    // 16x16 in one CTA: +24 %)
+    const bool split = SPLIT && blockDim.x > 32u && gridDim.x > 1u;
 
     const uint32_t i = threadIdx.x, lane = i & 31u;
     const TileShape T = tile_shape(S, tile);
@@ -342,7 +378,11 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
     {
         const uint32_t nsm = NCOUNTERS + (smem_hist ? 3u * S.nb : 0u);
         for (uint32_t k = i; k < nsm; k += blockDim.x) scnt[k] = 0u;
-        if (i == 0) { s_abort = 0; s_busy[0] = s_busy[1] = 0u; }
+        if (i == 0) {
+            s_abort = 0;
+            s_busy[0] = s_busy[1] = 0u;
+            if (split) mbar_init(mbar, blockDim.x / 32u);
+        }
     }
     // shared-window addresses: flit slot d of node slot j at parity b is
     // fa + b*FSTR + (d*np + j)*16; its occupancy byte oa + b*OSTR + j*4 + d
@@ -547,7 +587,15 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         const uint32_t st = (uint32_t)t, stn = st + 1u;
         const bool last = cc + 1u == ncyc;
         bool busy = false;
+        // split barrier: every warp's link stores of cycle t-1 are visible
+        if (split && cc > 0u) {
+            mbar_wait(mbar, (cc - 1u) & 1u);
+            if (s_abort) break;
+        }
         TRACE_DECL
+        Flit gej = Flit{0, 0, 0, 0};   // the flit ejected this cycle (<= 1)
+        bool ej = false;
+        uint32_t usedo = 0;
         if (active) {
             const unsigned long long *const llp = S.ll + (size_t)pb * pstride;   // this cycle's boundary inputs
             // (1) latch.  Slots 0..3 = link inputs N,S,E,W,
@@ -793,16 +841,30 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                     sts8_if(go, no + (w >> 16));
                 }
             }
+            if (has_ej) {
+                gej = pick5(f, (inv >> 16) & 15u);
+                ej = true;
+            }
+            usedo = used;
+        }
+        // split barrier: this warp's link stores of cycle t are done.  What
+        // follows (Phase 3 of t, Phase 1 of t+1) is node-local, so it
+        // overlaps the other warps' routing and the boundary-input latency
+        // instead of extending every warp's cycle
+        if (split) {
+            __syncwarp();
+            if (lane == 0u) mbar_arrive(mbar);
+        }
+        if (active) {
             // (5) Phase 3: the ejected flit (<= 1) is delivered and
             // serviced now, after this cycle's outputs are out
-            if (has_ej) {
-                const Flit g = pick5(f, (inv >> 16) & 15u);
-                if (st - g.z > LIFE_MAX) errf |= ERR_AGE;   // R32
+            if (ej) {
+                if (st - gej.z > LIFE_MAX) errf |= ERR_AGE;   // R32
                 TRACE_EV(1u);
-                phase3(S, K, c, g, t, acc);
+                phase3(S, K, c, gej, t, acc);
                 if (windows) wake = wake_from(st);
             }
-            if (DRAIN) busy = used != 0u || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
+            if (DRAIN) busy = usedo != 0u || q_count(c.qctl) > 0u || core_mode(c.hot) != MIDLE;
         }
         TRACE_P3_DONE
         // (6) Phase 1 of cycle t+1, after the draw windows it needs
@@ -836,10 +898,12 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         // memory link stores before the next cycle's loads.
         if (DRAIN && busy) s_busy[cc & 1u] = cc + 1u;
         if (CL) cluster_barrier();
-        else __syncthreads();
+        else if (!split) __syncthreads();
         if (DRAIN && i == 0 && s_busy[cc & 1u] == cc + 1u) atomicAdd(&activity[cc], 1u);
-        if (s_abort) break;
+        if (!split && s_abort) break;
     }
+    // the last cycle's link stores of every warp before the spill reads them
+    if (split) __syncthreads();
 
     // ---- epilogue: spill state
     const uint64_t tend = t0 + ncyc;

@@ -674,3 +674,27 @@ def test_cluster_exchange(cfg, monkeypatch):
     g, o = both(cfg, 2600, nb.ENGINE_TILED, split=[1, 600, 1999], drain=100000)
     assert g.info()["cluster"] > 1
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("engine", [nb.ENGINE_PERSIST, nb.ENGINE_TILED])
+def test_streamed_script_many_merges(engine):
+    """120 pushed pieces, each merged right before its events fall due (the
+    merge allocates, zeroes and fills count / offset buffers each time):
+    regression for a pushed piece lost when a buffer's legacy-stream zeroing
+    landed after the copy that filled it on the library's non-blocking stream.
+    Bit-exact against the oracle."""
+    cfg = W.lspd(16, 12, thr_inj=0, sendq_cap=64, l2_sets=2, mem_lat=20)
+    script = W.random_script(cfg, 6000, 2400, seed=71)
+    bounds = list(range(20, 2400, 20))
+    parts = _pieces(script, bounds)
+    g = nb.NocSim(cfg, script=parts[0], engine=engine)
+    o = Oracle(cfg, script=parts[0])
+    for piece in parts[1:]:
+        g.push_script(piece)
+        o.push_script(piece)
+        g.run(20)
+        o.run(20)
+    g.run(400)
+    o.run(400)
+    assert o.stats()[0]["accesses"] > 3000
+    assert_same(g, o)
