@@ -4,7 +4,10 @@
 
 namespace noc {
 
-constexpr uint32_t PERSIST_BLOCK = 256;
+#ifndef NOC_PERSIST_BLOCK
+#define NOC_PERSIST_BLOCK 256   // A/B builds: -DNOC_PERSIST_BLOCK=N
+#endif
+constexpr uint32_t PERSIST_BLOCK = NOC_PERSIST_BLOCK;
 // 3 co-resident PERSIST CTAs per SM (<= 80 registers): large meshes are DRAM-latency
 // bound and need the warps (A/B at C5: 24 vs 16 warps per SM, -18% per cycle)
 #ifndef NOC_PERSIST_MIN_BLOCKS
