@@ -173,7 +173,13 @@ def noc_sim_stats(h, nbins: int):
         d["drops_" + k] = cnt.drops[i]
     for n in L1_COUNTER_NAMES + MIG_COUNTER_NAMES + MEM_COUNTER_NAMES:
         d[n] = getattr(cnt, n)
-    return d, list(hl), list(hd), list(ha)
+    # memoryview -> list converts in C (list() over a ctypes array boxes each
+    # element through ctypes: 0.7 ms of a 6.6 ms C3 step, measured)
+    return d, _u64_list(hl), _u64_list(hd), _u64_list(ha)
+
+
+def _u64_list(a) -> list:
+    return memoryview(a).cast("B").cast("Q").tolist()
 
 
 def noc_sim_state_hash(h) -> int:
