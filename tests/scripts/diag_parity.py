@@ -4,7 +4,7 @@ usage: python tools/diag_parity.py [case]"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1508_03235_b200 as nb  # noqa: E402
 from paper_1508_03235_b200 import workloads as W  # noqa: E402
 from oracle import Oracle  # noqa: E402
