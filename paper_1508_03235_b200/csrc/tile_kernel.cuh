@@ -74,30 +74,64 @@ __device__ __forceinline__ TileShape tile_shape(const Dev &S, uint32_t b)
 // Thread <-> node mapping inside a tile: the interior nodes (no boundary port)
 // take the first threads/warps, the boundary ring the last ones, so the warps
 // of interior nodes never execute (or wait in) the boundary-exchange code.
-__device__ __forceinline__ void tile_pos(const TileShape &T, uint32_t i, uint32_t &lx, uint32_t &ly)
+// The ring starts at the first warp boundary after the interior and is spread
+// evenly over its warps (`per` lanes each; C3's 30x10 tiles: 76 ring nodes as
+// 26 + 25 + 25 instead of 32 + 32 + 12) when the block has room for it:
+// the ring warps are the cycle's critical path, and a warp with fewer nodes
+// meets fewer of the rare, long per-node events each cycle.
+struct RingMap {
+    uint32_t ic;    // interior nodes (threads 0 .. ic-1)
+    uint32_t rs;    // first ring thread
+    uint32_t per;   // ring nodes per ring warp
+};
+__device__ __forceinline__ RingMap ring_map(const TileShape &T, uint32_t np)
 {
-    if (T.tw < 3 || T.th < 3) { lx = i % T.tw; ly = i / T.tw; return; }
-    const uint32_t iw = T.tw - 2, ic = iw * (T.th - 2);
-    if (i < ic) { lx = 1 + i % iw; ly = 1 + i / iw; return; }
-    uint32_t j = i - ic;
-    if (j < T.tw) { lx = j; ly = 0; return; }
-    j -= T.tw;
-    if (j < T.tw) { lx = j; ly = T.th - 1; return; }
-    j -= T.tw;
-    if (j < T.th - 2) { lx = 0; ly = 1 + j; return; }
-    j -= T.th - 2;
-    lx = T.tw - 1; ly = 1 + j;
+    RingMap m;
+    if (T.tw < 3 || T.th < 3) { m.ic = 0; m.rs = 0; m.per = 32; return m; }   // all ring, linear
+    m.ic = (T.tw - 2) * (T.th - 2);
+    const uint32_t ring = T.tn - m.ic;
+    const uint32_t rs = (m.ic + 31u) & ~31u, nw = (ring + 31u) / 32u;
+#ifndef NOC_NO_RING_BALANCE
+    if (rs + 32u * nw <= np) { m.rs = rs; m.per = (ring + nw - 1u) / nw; return m; }
+#endif
+    m.rs = m.ic;   // contiguous
+    m.per = 32u;
+    return m;
 }
 
-__device__ __forceinline__ uint32_t tile_slot(const TileShape &T, uint32_t lx, uint32_t ly)
+// node of thread i (false: no node, a padding lane)
+__device__ __forceinline__ bool tile_pos(const TileShape &T, const RingMap &M, uint32_t i, uint32_t &lx, uint32_t &ly)
+{
+    if (T.tw < 3 || T.th < 3) { lx = i % T.tw; ly = i / T.tw; return i < T.tn; }
+    const uint32_t iw = T.tw - 2;
+    if (i < M.ic) { lx = 1 + i % iw; ly = 1 + i / iw; return true; }
+    if (i < M.rs) return false;
+    const uint32_t r = i - M.rs, ln = r & 31u;
+    if (ln >= M.per) return false;
+    uint32_t j = (r >> 5) * M.per + ln;
+    if (j >= T.tn - M.ic) return false;
+    if (j < T.tw) { lx = j; ly = 0; return true; }
+    j -= T.tw;
+    if (j < T.tw) { lx = j; ly = T.th - 1; return true; }
+    j -= T.tw;
+    if (j < T.th - 2) { lx = 0; ly = 1 + j; return true; }
+    j -= T.th - 2;
+    lx = T.tw - 1; ly = 1 + j;
+    return true;
+}
+
+// thread of node (lx, ly)
+__device__ __forceinline__ uint32_t tile_slot(const TileShape &T, const RingMap &M, uint32_t lx, uint32_t ly)
 {
     if (T.tw < 3 || T.th < 3) return ly * T.tw + lx;
-    const uint32_t iw = T.tw - 2, ic = iw * (T.th - 2);
+    const uint32_t iw = T.tw - 2;
     if (lx >= 1 && lx + 1 < T.tw && ly >= 1 && ly + 1 < T.th) return (ly - 1) * iw + (lx - 1);
-    if (ly == 0) return ic + lx;
-    if (ly + 1 == T.th) return ic + T.tw + lx;
-    if (lx == 0) return ic + 2 * T.tw + (ly - 1);
-    return ic + 2 * T.tw + (T.th - 2) + (ly - 1);
+    uint32_t j;
+    if (ly == 0) j = lx;
+    else if (ly + 1 == T.th) j = T.tw + lx;
+    else if (lx == 0) j = 2 * T.tw + (ly - 1);
+    else j = 2 * T.tw + (T.th - 2) + (ly - 1);
+    return M.rs + (j / M.per) * 32u + j % M.per;
 }
 
 __device__ __forceinline__ void ld_relaxed_sys_x2(const unsigned long long *p, unsigned long long &a,
@@ -373,7 +407,9 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 
     const uint32_t i = threadIdx.x, lane = i & 31u;
     const TileShape T = tile_shape(S, tile);
-    const bool active = i < T.tn;
+    const RingMap RM = ring_map(T, blockDim.x);
+    uint32_t lx = 0, lyy = 0;
+    const bool active = tile_pos(T, RM, i, lx, lyy);
 
     {
         const uint32_t nsm = NCOUNTERS + (smem_hist ? 3u * S.nb : 0u);
@@ -392,8 +428,6 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
 
     // ---- node registers (persist for the whole launch)
     NodeCtx c;
-    uint32_t lx = 0, lyy = 0;
-    if (active) tile_pos(T, i, lx, lyy);
     c.x = T.x0 + lx;
     c.y = T.y0 + lyy;
     c.n = c.y * S.W + c.x;
@@ -435,10 +469,10 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
         for (uint32_t d = 0; d < 4; ++d) {
             uint32_t m = c.l, mi = 0;
             switch (d) {
-            case PN: m = c.l - S.W; if ((intl >> d) & 1u) mi = tile_slot(T, lx, lyy - 1); break;
-            case PS: m = c.l + S.W; if ((intl >> d) & 1u) mi = tile_slot(T, lx, lyy + 1); break;
-            case PE: m = c.l + 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx + 1, lyy); break;
-            default: m = c.l - 1u; if ((intl >> d) & 1u) mi = tile_slot(T, lx - 1, lyy); break;
+            case PN: m = c.l - S.W; if ((intl >> d) & 1u) mi = tile_slot(T, RM, lx, lyy - 1); break;
+            case PS: m = c.l + S.W; if ((intl >> d) & 1u) mi = tile_slot(T, RM, lx, lyy + 1); break;
+            case PE: m = c.l + 1u; if ((intl >> d) & 1u) mi = tile_slot(T, RM, lx + 1, lyy); break;
+            default: m = c.l - 1u; if ((intl >> d) & 1u) mi = tile_slot(T, RM, lx - 1, lyy); break;
             }
             if ((intl >> d) & 1u) na[d] = (((d ^ 1u) * np + mi) * 16u) | ((mi * 4u + (d ^ 1u)) << 16);
             sna[d * np + i] = na[d];
@@ -448,7 +482,7 @@ k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t s
                 const uint32_t vy = c.y + (d == PS ? 1u : 0u) - (d == PN ? 1u : 0u);
                 const uint32_t rb = tile_of(vy - S.row0, S.rows, S.TY) * S.TX + tile_of(vx, S.W, S.TX);
                 const TileShape R = tile_shape(S, rb);
-                const uint32_t mr = tile_slot(R, vx - R.x0, vy - R.y0);
+                const uint32_t mr = tile_slot(R, ring_map(R, blockDim.x), vx - R.x0, vy - R.y0);
                 ExtIn e;
                 e.port = d;
                 e.inw = rb;
