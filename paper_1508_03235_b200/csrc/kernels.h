@@ -14,8 +14,20 @@ constexpr uint32_t PERSIST_BLOCK = NOC_PERSIST_BLOCK;
 #define NOC_PERSIST_MIN_BLOCKS 3   // A/B builds: -DNOC_PERSIST_MIN_BLOCKS=N
 #endif
 constexpr uint32_t PERSIST_MIN_BLOCKS = NOC_PERSIST_MIN_BLOCKS;
-constexpr uint32_t TILE_BLOCK_MAX = 320;                  // nodes (= threads) per CTA: C3 tiles are 300; 320 leaves 204 registers (A/B: -2.7 % per cycle vs 512)
+constexpr uint32_t TILE_BLOCK_MAX = 320;                  // nodes per CTA: C3 tiles are 300 (the 320 cap beat 512 by 2.7 % in round 1)
 constexpr uint32_t TILE_MIN_BLOCKS = 1;                   // co-resident CTAs per SM
+// boundary-ring nodes per ring warp at most (tile_kernel.cuh ring_map); below
+// 32 the block gets extra ring warps, up to TILE_THREADS_MAX threads
+#ifndef NOC_RING_CAP
+#define NOC_RING_CAP 16
+#endif
+constexpr uint32_t TILE_RING_CAP = NOC_RING_CAP;
+#ifndef NOC_TILE_THREADS
+#define NOC_TILE_THREADS (NOC_RING_CAP >= 32 ? 320 : NOC_RING_CAP >= 20 ? 352 : NOC_RING_CAP >= 16 ? 384 : 416)
+#endif
+constexpr uint32_t TILE_THREADS_MAX = NOC_TILE_THREADS;   // launch bound
+// (ring cap A/B, profiles/r02_ab_split_barrier.txt: 16 -> C3 -3 %, C2 -20 % against one 32-lane ring
+// warp sequence; 12 squeezes the kernel to 128 registers and is slower)
 
 // Row bands handled by one process (virtual bands on one GPU, or the single
 // band of a rank); every band's tiles run in one cooperative launch.

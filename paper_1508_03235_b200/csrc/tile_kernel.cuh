@@ -90,9 +90,11 @@ __device__ __forceinline__ RingMap ring_map(const TileShape &T, uint32_t np)
     if (T.tw < 3 || T.th < 3) { m.ic = 0; m.rs = 0; m.per = 32; return m; }   // all ring, linear
     m.ic = (T.tw - 2) * (T.th - 2);
     const uint32_t ring = T.tn - m.ic;
-    const uint32_t rs = (m.ic + 31u) & ~31u, nw = (ring + 31u) / 32u;
+    const uint32_t rs = (m.ic + 31u) & ~31u, nw0 = (ring + 31u) / 32u;
+    const uint32_t avail = np > rs ? (np - rs) / 32u : 0u;
+    const uint32_t nw = min((ring + TILE_RING_CAP - 1u) / TILE_RING_CAP, avail);
 #ifndef NOC_NO_RING_BALANCE
-    if (rs + 32u * nw <= np) { m.rs = rs; m.per = (ring + nw - 1u) / nw; return m; }
+    if (nw >= nw0 && nw > 0u) { m.rs = rs; m.per = (ring + nw - 1u) / nw; return m; }
 #endif
     m.rs = m.ic;   // contiguous
     m.per = 32u;
@@ -362,7 +364,7 @@ constexpr uint32_t NOPORT = 8u;
 // MODE: 0 uniform random, 1 LSPD, 2 LSPD with the NEXT-f1 private L1 (the L1
 // timer checks compiled in only there)
 template <uint32_t MODE, bool DRAIN, uint32_t FEAT>
-__global__ void __launch_bounds__(TILE_BLOCK_MAX, TILE_MIN_BLOCKS)
+__global__ void __launch_bounds__(TILE_THREADS_MAX, TILE_MIN_BLOCKS)
 k_tiled(const __grid_constant__ DevSet P, uint64_t t0, uint32_t ncyc, uint32_t smem_hist, uint32_t *activity)
 {
     constexpr uint32_t FULL = 0xFFFFFFFFu;
