@@ -19,15 +19,16 @@ constexpr uint32_t TILE_MIN_BLOCKS = 1;                   // co-resident CTAs pe
 // boundary-ring nodes per ring warp at most (tile_kernel.cuh ring_map); below
 // 32 the block gets extra ring warps, up to TILE_THREADS_MAX threads
 #ifndef NOC_RING_CAP
-#define NOC_RING_CAP 16
+#define NOC_RING_CAP 4
 #endif
 constexpr uint32_t TILE_RING_CAP = NOC_RING_CAP;
 #ifndef NOC_TILE_THREADS
-#define NOC_TILE_THREADS (NOC_RING_CAP >= 32 ? 320 : NOC_RING_CAP >= 20 ? 352 : NOC_RING_CAP >= 16 ? 384 : 416)
+#define NOC_TILE_THREADS (NOC_RING_CAP >= 32 ? 320 : 384)
 #endif
-constexpr uint32_t TILE_THREADS_MAX = NOC_TILE_THREADS;   // launch bound
-// (ring cap A/B, profiles/r02_ab_split_barrier.txt: 16 -> C3 -3 %, C2 -20 % against one 32-lane ring
-// warp sequence; 12 squeezes the kernel to 128 registers and is slower)
+constexpr uint32_t TILE_THREADS_MAX = NOC_TILE_THREADS;   // launch bound (384: <= 170 registers, 157 used)
+// (A/B, profiles/r02_ab_split_barrier.txt: a 384-thread CTA gives C3's 76 ring nodes 5 warps of <= 16,
+// C3 -3 %; C2's 30-node tiles get an interior warp and 5 ring warps of <= 4, C2 -27 % (cap 8: -25 %); 416 threads
+// squeeze the kernel to 128 registers and are slower)
 
 // Row bands handled by one process (virtual bands on one GPU, or the single
 // band of a rank); every band's tiles run in one cooperative launch.
